@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the DSEAmd hot path (arXiv 2507.11289) on B200.
+
+Metric (BASELINE.json; §4.3): atom-timesteps/s = molecules processed by all
+workers in one super-cycle / super-cycle time.  One bench "step" is one super-cycle
+(N_w = N_GPU * W timesteps of every atom: force, kick, drift, migration, finalise
+and ring hop of every slice -- all §8(a) rows).
+
+Default workload: C4 of BASELINE.json (16,384,000-atom LJ cube, rho* 0.8, T* 1.0,
+rc 2.5, 109 slices; strong scaling at 1/2/4/8 GPUs).  Inputs are larger than L2
+(1.25 GB of state), so no L2 flush is needed between steps.  Before the warm-up the
+lattice is melted for --equil timesteps (untimed; the perfect lattice has
+unrealistically uniform cell occupancy).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl dsea|reference]
+  N > 1: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+--impl reference times the CPU oracle (oracle/, O(N^2) all pairs) on the host cores on
+a bounded sample of the same workload: each step computes the Algorithm 1 forces of a
+sample of atoms against all N atoms.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# bytes one atom costs the fused force+integrate kernel at minimum: read r, v, F_old (72 B)
+# + id (4 B); write r', v', F_new (72 B) + id (4 B) + destination key (4 B)
+FORCE_BYTES_PER_ATOM = 156
+# FP64 flops of Algorithm 1 per in-cutoff ordered pair (FMA = 2)
+FP64_FLOPS_PER_PAIR = 33
+FP64_LANES_PER_SM = 64
+N_SMS = 148
+
+
+def peaks():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 1965.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_rate(cfg, seconds_target=15.0, max_sample=None):
+    """Time the oracle (as it stands) on the host cores: Algorithm 1 forces of a sample
+    of atoms against all N atoms (the O(N) per-atom work of its O(N^2) step)."""
+    import numpy as np
+    import oracle
+    g = oracle.geometry(cfg.nx, cfg.ny, cfg.nz, cfg.rho, cfg.rc, cfg.n_slices, cfg.cells_per_slice_x)
+    x = oracle.lattice(cfg.nx, cfg.ny, cfg.nz, g.a)
+    n = x.shape[0]
+    threads = oracle.default_threads()
+    rng = np.random.default_rng(0)
+    k = 8
+    while True:
+        idx = np.sort(rng.choice(n, min(k, n), replace=False))
+        t0 = time.perf_counter()
+        oracle.forces_subset(x, g.b, cfg.rc, idx, threads)
+        dt = time.perf_counter() - t0
+        if dt > seconds_target / 4 or k >= n or (max_sample and k >= max_sample):
+            break
+        k = min(n, int(k * max(2.0, (seconds_target / 4) / max(dt, 1e-4))))
+    # final timed sample sized for ~seconds_target
+    k = min(n, max(k, int(k * seconds_target / max(dt, 1e-4) / 2)))
+    if max_sample:
+        k = min(k, max_sample)
+    idx = np.sort(rng.choice(n, k, replace=False))
+    t0 = time.perf_counter()
+    oracle.forces_subset(x, g.b, cfg.rc, idx, threads)
+    dt = time.perf_counter() - t0
+    return k / dt, threads, k, dt
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle, timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    g = oracle.geometry(cfg.nx, cfg.ny, cfg.nz, cfg.rho, cfg.rc, cfg.n_slices, cfg.cells_per_slice_x)
+    x = oracle.lattice(cfg.nx, cfg.ny, cfg.nz, g.a)
+    n = x.shape[0]
+    threads = oracle.default_threads()
+    # size one step for ~ 8 s so warmup + steps ends within a few minutes
+    rate, _, _, _ = cpu_oracle_rate(cfg, seconds_target=4.0)
+    per_step = int(max(1, min(n, rate * 8.0 / max(1, args.steps + args.warmup) * 4)))
+    per_step = max(1, min(per_step, n))
+    rng = np.random.default_rng(1)
+    for _ in range(args.warmup):
+        idx = np.sort(rng.choice(n, per_step, replace=False))
+        oracle.forces_subset(x, g.b, cfg.rc, idx, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        idx = np.sort(rng.choice(n, per_step, replace=False))
+        oracle.forces_subset(x, g.b, cfg.rc, idx, threads)
+    dt = time.perf_counter() - t0
+    value = per_step * args.steps / dt
+    sample = (f"per step: Algorithm 1 forces of {per_step} sampled atoms of {n:,} against all {n:,} "
+              f"(all-pairs O(N) each, minimum image y/z) on the {cfg.name} lattice")
+    line = {"metric": "atom-timesteps/s", "value": value, "unit": "atom-timesteps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (FCC lattice, seeded velocities)",
+            "config": {"workload": cfg.name, "n_atoms": n, "n_slices": g.n_slices, "rho": cfg.rho,
+                       "rc": cfg.rc},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "atom-timesteps/s", "cores": threads,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "atom-timesteps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="dsea", choices=["dsea", "reference"])
+    ap.add_argument("--workers", type=int, default=1)
+    ap.add_argument("--equil", type=int, default=200, help="untimed melting timesteps before warm-up")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    from paper_2507_11289_b200 import CONFIGS
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    from paper_2507_11289_b200 import dsea as D
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    W = args.workers
+    e = D.Engine(D.Box(cfg.nx, cfg.ny, cfg.nz, cfg.rho, cfg.rc, cfg.dt, cfg.T0, cfg.seed))
+    e.slice(n_slices=cfg.n_slices, cells_per_slice_x=cfg.cells_per_slice_x, n_gpus=world, rank=rank,
+            device=local_rank, workers_per_gpu=W)
+    if world > 1:
+        ids = [b"".join(D.dsea_ring_unique_id() for _ in range(world))] if rank == 0 else [None]
+        dist.broadcast_object_list(ids, src=0)
+        D.dsea_ring_connect(e.ctx, ids[0], world)
+    geo = e.geometry
+    nw = world * W
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # melt the lattice (untimed), then warm up (untimed)
+    if args.equil > 0:
+        e.step(((args.equil + nw - 1) // nw) * nw)
+    barrier()
+    for _ in range(args.warmup):
+        e.step(nw)
+    barrier()
+
+    # ---- timed region: K super-cycles, device-timed with CUDA events ----------------
+    D.dsea_reset_stats(e.ctx)
+    D.dsea_set_timing(e.ctx, True)
+    hbm_peak, sm_max, peak_kind = peaks()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        e.step(args.steps * nw)
+        ev1.record()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    st = e.stats()
+    D.dsea_set_timing(e.ctx, False)
+    t = torch.tensor([ms, float(st.kernel_launches)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tmax[1:], op=dist.ReduceOp.SUM)
+        t = tmax
+    ms_total = float(t[0])
+    launches = int(t[1])
+    atoms = int(geo.n_atoms)
+    value = atoms * args.steps * nw / (ms_total * 1e-3)
+
+    # dominant kernel: fused force+integrate (per-launch average on its own stream)
+    force_ms_avg = st.force_ms / max(1, st.force_launches)
+    atoms_per_launch = atoms if world == 1 and W == 1 else atoms / geo.n_slices
+    pairs_per_atom = st.force_pairs / max(1, atoms)
+    fp64_peak = N_SMS * FP64_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12  # TFLOP/s
+    fp64_achieved = pairs_per_atom * atoms_per_launch * FP64_FLOPS_PER_PAIR / (force_ms_avg * 1e-3) / 1e12
+    hbm_achieved = FORCE_BYTES_PER_ATOM * atoms_per_launch / (force_ms_avg * 1e-3) / 1e9
+    force_share = st.force_ms / max(1e-9, st.force_ms + st.bin_ms)
+
+    # ---- e2e through the public API with host buffers ------------------------------
+    e2e = None
+    if not args.no_e2e:
+        xh = e.positions() if rank == 0 else np.zeros((atoms, 3))
+        vh = e.velocities() if rank == 0 else np.zeros((atoms, 3))
+        xh = np.ascontiguousarray(xh)
+        vh = np.ascontiguousarray(vh)
+        barrier()
+        t0 = time.perf_counter()
+        e.set_state(xh, vh)                       # H2D of the inputs + device binning
+        e.step(args.steps * nw)
+        if rank == 0:
+            xo = e.positions()                    # D2H of the result
+            _ = e.energies()
+        barrier()
+        dt = time.perf_counter() - t0
+        if dist is not None:
+            tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt[0])
+        e2e = {"value": atoms * args.steps * nw / dt, "unit": "atom-timesteps/s",
+               "h2d_bytes_per_step": int(atoms * 48 / args.steps),
+               "d2h_bytes_per_step": int((atoms * 24 + args.steps * nw * 32) / args.steps),
+               "note": "set_state(host r, v) + step(K super-cycles) + get_positions + energies; "
+                       "bytes amortised over the K steps"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cores, k, secs = cpu_oracle_rate(cfg, seconds_target=15.0)
+        cpu = {"value": rate, "unit": "atom-timesteps/s", "cores": cores, "kind": "oracle",
+               "sample": f"Algorithm 1 forces of {k} sampled atoms of {atoms:,} against all atoms "
+                         f"(O(N^2) oracle, {secs:.1f} s on {cores} threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": "atom-timesteps/s", "value": value, "unit": "atom-timesteps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: FCC lattice (P:224) + seeded Maxwell-Boltzmann velocities, "
+                    f"melted {args.equil} steps",
+            "config": {"workload": cfg.name, "n_atoms": atoms, "n_slices": geo.n_slices,
+                       "cells": list(geo.cells), "rho": cfg.rho, "rc": cfg.rc, "dt": cfg.dt,
+                       "workers_per_gpu": W, "timesteps_per_step": nw,
+                       "mode": "fused" if world == 1 and W == 1 else "staged-ring",
+                       "l2": "inputs larger than L2 (state %.2f GB)" % (atoms * 76 / 1e9),
+                       "parallelism": f"ring{world}"},
+            "roofline": {"bound": "alu", "achieved": fp64_achieved, "peak": fp64_peak,
+                         "unit": "TFLOP/s", "frac": fp64_achieved / fp64_peak, "traffic": None,
+                         "kernel": "k_force (force + kick + drift + migration key)",
+                         "peak_note": f"FP64: {N_SMS} SMs x {FP64_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz",
+                         "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                                 "frac": hbm_achieved / hbm_peak, "peak_kind": peak_kind,
+                                 "bytes_per_atom": FORCE_BYTES_PER_ATOM},
+                         "force_ms_per_launch": force_ms_avg, "force_share_of_step": force_share,
+                         "pairs_per_atom": pairs_per_atom},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    e.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

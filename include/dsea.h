@@ -1,0 +1,213 @@
+/*
+ * dsea.h -- C ABI of the B200-native DSEAmd slice-streaming engine
+ * (arXiv 2507.11289, "Cyclic Data Streaming on GPUs for Short Range Stencils
+ * Applied to Molecular Dynamics").  Library: paper_2507_11289_b200/libdsea.so.
+ *
+ * Citations: P:n = PAPER.md line n, with the section / equation / algorithm.
+ * Readings of passages the paper leaves open are listed in DESIGN.md §3 (Q1-Q19).
+ *
+ * The calls follow the paper's problem statement: prepare slices of the dataset
+ * (§3), run super-cycles in which every worker advances every slice one
+ * timestep (§3.1), store the slices, with the LJ case of §4:
+ * box, density and cutoff, Algorithm 1 stepping.
+ *
+ * Conventions (all calls):
+ *  - Every call returns dsea_status: 0 = OK, < 0 = error.  No C++ exception
+ *    crosses the ABI.  After an error, dsea_last_error(ctx) names the cause.
+ *  - The library owns every device allocation.  The caller owns every host
+ *    array passed in; the library never keeps a caller pointer past the call.
+ *  - Per-atom host arrays are ordered by atom id, AoS, 3 doubles per atom:
+ *    id = ((ix*ny + iy)*nz + iz)*4 + k for FCC cell (ix,iy,iz) and basis site k.
+ *  - A context is not thread-safe; distinct contexts are independent.
+ *  - One context drives one GPU (one process per GPU).  A ring of N_GPU GPUs is
+ *    N_GPU processes, each with its own context, connected by dsea_ring_connect.
+ *  - Units: reduced LJ units, sigma = epsilon = m = k_B = 1.
+ *  - There is no CPU fallback: calls that need a GPU return DSEA_ECUDA when
+ *    no device is usable.
+ */
+#ifndef DSEA_H
+#define DSEA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dsea_ctx dsea_ctx; /* opaque; owns all device memory */
+
+typedef enum {
+    DSEA_OK = 0,
+    DSEA_EINVAL = -1,    /* bad argument: null pointer, n < 1, rho <= 0, rc <= 0, dt <= 0,
+                            short buffer, atom outside the box in dsea_set_state */
+    DSEA_EGEOM = -2,     /* infeasible geometry: slice width < rc, cell edge < rc, fewer
+                            than 3 cells in y or z, or (single GPU, staged) N_S < 2 + 2W */
+    DSEA_ESTATE = -3,    /* call order: step before slice, read-back on a rank that does
+                            not hold the state, ring not connected */
+    DSEA_ECAPACITY = -4, /* a slice outgrew its padded slot capacity, or a force tile its
+                            shared-memory staging (message names slice and timestep) */
+    DSEA_EUNSTABLE = -5, /* an atom moved more than one slice in one step, or a non-finite
+                            position (message names atom id and timestep) */
+    DSEA_ECUDA = -6,     /* CUDA runtime error or no usable device */
+    DSEA_ENOMEM = -7,    /* device or host allocation failed */
+    DSEA_EPEER = -8      /* NCCL unavailable or ring setup / transfer failed */
+} dsea_status;
+
+/* Box and run parameters (§4).  The box holds nx*ny*nz FCC
+ * unit cells of edge a = (4/rho)^(1/3): b_d = n_d * a, N = 4*nx*ny*nz.  x is the
+ * slicing axis and carries the mirror walls (§3, §4.2); y and z are
+ * periodic (Q1).  The paper's cube is nx = ny = nz = N_i. */
+typedef struct {
+    int32_t nx, ny, nz; /* FCC unit cells per axis, each >= 1 */
+    double rho;         /* density rho*sigma^3 > 0 */
+    double rc;          /* cutoff radius > 0 (paper: 2.5) */
+    double dt;          /* timestep > 0 (paper: ~1.8e-3; Q8: 0.0018) */
+    double T0;          /* initial temperature for the velocity draw (Q9) */
+    uint64_t seed;      /* splitmix64 seed of the velocity draw (Q9) */
+} dsea_box_params;
+
+/* Slicing and ring parameters (§3, §3.1). */
+typedef struct {
+    int32_t n_slices;          /* N_S; 0 -> paper rule floor(b_x / (c*rc)) */
+    int32_t cells_per_slice_x; /* c >= 1 cells across a slice (paper: 1) */
+    int32_t n_gpus;            /* N_GPU = ring length = number of processes, >= 1 */
+    int32_t rank;              /* this process's ring position, 0 <= rank < n_gpus */
+    int32_t device;            /* CUDA device ordinal for this context */
+    int32_t workers_per_gpu;   /* W = N_wGPU >= 1 */
+    int32_t mode;              /* DSEA_MODE_* below */
+    double capacity_factor;    /* slot capacity / mean atoms per slice; 0 -> 1.25 */
+} dsea_slice_params;
+
+#define DSEA_MODE_AUTO 0   /* FUSED when n_gpus == 1 and W == 1, else STAGED */
+#define DSEA_MODE_FUSED 1  /* n_gpus == 1, W == 1: all stages of a super-cycle fused into
+                              one force launch and one bin pass (same results bitwise) */
+#define DSEA_MODE_STAGED 2 /* the paper's per-stage schedule (Table 1),
+                              generalised to W workers per GPU and N_GPU GPUs */
+
+/* Derived geometry (valid after dsea_slice; dsea_geometry_compute gives it without
+ * a context).  cells[0] = c * n_slices. */
+typedef struct {
+    double b[3];       /* box edges */
+    double l[3];       /* cell edges, each >= rc */
+    double w;          /* slice width b_x / N_S */
+    double a;          /* FCC lattice constant */
+    double u_shift;    /* rc^-6 - rc^-12 (Q6) */
+    int32_t cells[3];  /* cells per axis */
+    int32_t n_slices;  /* N_S */
+    int32_t n_max;     /* Eq. (1): N_S / (2 + W*(O_in+O_out)), O = 1 */
+    int32_t slot_capacity; /* atoms per slot (padded) */
+    int64_t n_atoms;   /* N */
+} dsea_geometry;
+
+/* Per-timestep observables (Alg. 1; Q12: E = U(r_n) + KE(v_n)).
+ * p = rho*T + 8 V / Vol with T = 2 KE / (3N). */
+typedef struct {
+    int64_t step;      /* absolute timestep index since dsea_init (0-based) */
+    double U;          /* potential energy, sum over ordered pairs of 4(...)/2 */
+    double KE;         /* kinetic energy after the velocity update of the same step */
+    double V;          /* virial accumulator of Alg. 1 */
+} dsea_energy;
+
+/* Counters for the benchmark harness (filled by dsea_get_stats). */
+typedef struct {
+    int64_t kernel_launches;   /* kernels this context launched since the last reset */
+    int64_t force_launches;    /* of which force-kernel launches */
+    int64_t atom_steps;        /* atom-timesteps processed by this rank */
+    double force_ms;           /* summed CUDA-event time of force launches (timing enabled) */
+    double bin_ms;             /* summed CUDA-event time of bin passes (timing enabled) */
+    double hop_ms;             /* summed CUDA-event time of ring sends (timing enabled) */
+    int64_t hop_bytes;         /* bytes sent to the ring successor */
+    int64_t force_pairs;       /* in-cutoff ordered pairs evaluated (from the last step) */
+} dsea_stats;
+
+/* ---- lifecycle ---------------------------------------------------------------- */
+
+/* Validate the box parameters, compute a and b, generate the FCC lattice
+ * (offset a/4: Q10) and the velocities (Q9) on the host.
+ * No device work.  *out receives a new context (NULL on error). */
+dsea_status dsea_init(const dsea_box_params *box, dsea_ctx **out);
+
+/* Validate the slicing (requirements (1)-(3) of P:63-73; l >= rc; >= 3
+ * cells in y and z), bind the CUDA device, allocate the slot pools, bin the
+ * host state into cell-sorted slices on the device and keep them resident on
+ * rank 0 (replaces the round-robin load of P:93).  A ring with N_GPU > N_max
+ * is legal (it runs at the Eq. (1) plateau) and only noted in
+ * dsea_last_error.  May be called again to re-slice. */
+dsea_status dsea_slice(dsea_ctx *ctx, const dsea_slice_params *sp);
+
+/* n_gpus > 1 only: connect this rank to its ring neighbours with NCCL
+ * point-to-point links.  ids = n_gpus consecutive 128-byte ncclUniqueId blobs;
+ * link r carries slices from rank r to rank (r+1) mod n_gpus.  Every rank must
+ * pass the same ids (create them on rank 0 with dsea_ring_unique_id and
+ * broadcast).  Collective over the ring: all ranks call it. */
+dsea_status dsea_ring_connect(dsea_ctx *ctx, const void *ids, int32_t n_ids);
+
+/* Write one fresh 128-byte ncclUniqueId into out (out_bytes >= 128). */
+dsea_status dsea_ring_unique_id(void *out, size_t out_bytes);
+
+/* Advance the system n_steps timesteps (n_steps >= 0) by streaming the slices
+ * through the ring of workers: ceil(n_steps / N_w) super-cycles of N_w =
+ * N_GPU*W timesteps, the trailing workers of a partial last
+ * super-cycle passing slices through unchanged (Q15).  Blocking: returns after
+ * every GPU is idle; afterwards the state rests on rank 0.  Collective over the
+ * ring: all ranks call it with the same n_steps. */
+dsea_status dsea_step(dsea_ctx *ctx, int64_t n_steps);
+
+void dsea_destroy(dsea_ctx *ctx); /* NULL-safe; frees all device memory */
+
+/* Message of the last error or warning on ctx; valid until the next call on ctx.
+ * Never NULL. */
+const char *dsea_last_error(const dsea_ctx *ctx);
+
+/* ---- state read-back and injection (rank 0 after dsea_step) ------------------ */
+
+dsea_status dsea_get_geometry(const dsea_ctx *ctx, dsea_geometry *out);
+
+/* xyz / vxyz / fxyz: caller-owned [3*n_atoms] arrays, filled by atom id.  Before
+ * dsea_slice these return the host-generated initial state.  fxyz is F_new of
+ * the last force pass (parity), zero before the first step. */
+dsea_status dsea_get_positions(dsea_ctx *ctx, double *xyz, int64_t n_atoms);
+dsea_status dsea_get_velocities(dsea_ctx *ctx, double *vxyz, int64_t n_atoms);
+dsea_status dsea_get_forces(dsea_ctx *ctx, double *fxyz, int64_t n_atoms);
+
+/* The engine's own binning of every atom as stored in the slot layout:
+ * cell_xyz[3*n] = global cell (x, y, z), slice[n] = slice index. */
+dsea_status dsea_get_cells(dsea_ctx *ctx, int32_t *cell_xyz, int32_t *slice, int64_t n_atoms);
+
+/* Energies of every timestep this rank computed since dsea_init, in step order.
+ * Writes min(cap, available) records; *n_written gets the count written. */
+dsea_status dsea_get_energies(dsea_ctx *ctx, dsea_energy *out, int64_t cap, int64_t *n_written);
+
+/* Replace the state (positions, velocities, optional F_new; NULL -> zero, the Q7
+ * convention) and re-bin on the device.  Positions must lie in [0,b_x] x [0,b_y)
+ * x [0,b_z).  On a multi-GPU ring only rank 0 stores it (other ranks: no-op). */
+dsea_status dsea_set_state(dsea_ctx *ctx, const double *xyz, const double *vxyz,
+                           const double *fxyz_or_null, int64_t n_atoms);
+
+/* ---- instrumentation ---------------------------------------------------------- */
+
+/* enable != 0: bracket every force launch, bin pass and send with CUDA events on
+ * the stream it runs on, summed into dsea_stats (costs one event pair per launch). */
+dsea_status dsea_set_timing(dsea_ctx *ctx, int32_t enable);
+dsea_status dsea_get_stats(dsea_ctx *ctx, dsea_stats *out);
+dsea_status dsea_reset_stats(dsea_ctx *ctx);
+
+/* ---- host-only helpers (no device needed; used by the CPU test suite) --------- */
+
+/* The geometry dsea_slice would derive (DSEA_EGEOM if infeasible, out still filled). */
+dsea_status dsea_geometry_compute(const dsea_box_params *box, const dsea_slice_params *sp,
+                                  dsea_geometry *out);
+
+/* The static stage schedule of one rank for n_cycles super-cycles (Table 1,
+ * P:153-171, generalised to W workers and N_GPU ranks; 1-based slice numbers as in
+ * the table).  Each row is 8 int32: {stage, recv, worker, process, bin, send,
+ * cycle, timestep} with -1 for "none"; one row per (stage, worker) pair that
+ * does something.  rows = NULL queries the count into *n_rows. */
+dsea_status dsea_schedule(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_t workers_per_gpu,
+                          int32_t n_cycles, int32_t *rows, int64_t cap_rows, int64_t *n_rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSEA_H */

@@ -1,0 +1,1000 @@
+// dsea_host.cpp -- C ABI, host-side initialisation and the ring runtime of the
+// B200-native DSEAmd engine (arXiv 2507.11289).  See include/dsea.h for the
+// contract of every entry point and DESIGN.md for the design.
+//
+//  - geometry and slicing ........ P:63-73 §3, §4 (readings Q3, Q18)
+//  - FCC lattice + velocities .... P:224-227 §4 (Q9, Q10); host, -ffp-contract=off
+//  - stage schedule .............. Table 1 (§3.3) generalised to W workers
+//                                  per GPU and N_GPU GPUs in a ring
+//  - ring hop .................... P:118-119 §3.1, §3.4: NCCL point-to-point
+//                                  over NVLink, one process per GPU
+//  - super-cycle ................. P:89-92 §3.1
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <new>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dsea.h"
+#include "dsea_internal.h"
+
+using namespace dsea;
+
+// ------------------------------------------------------------------------------
+// NCCL, loaded at run time (the process usually already has torch's copy).
+// ------------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl()
+{
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+#define LOADSYM(f, name) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, name))
+    LOADSYM(GetUniqueId, "ncclGetUniqueId");
+    LOADSYM(CommInitRank, "ncclCommInitRank");
+    LOADSYM(CommDestroy, "ncclCommDestroy");
+    LOADSYM(Send, "ncclSend");
+    LOADSYM(Recv, "ncclRecv");
+    LOADSYM(GroupStart, "ncclGroupStart");
+    LOADSYM(GroupEnd, "ncclGroupEnd");
+    LOADSYM(GetErrorString, "ncclGetErrorString");
+#undef LOADSYM
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
+             api.GroupStart && api.GroupEnd && api.GetErrorString;
+    return api;
+}
+
+// ------------------------------------------------------------------------------
+// Stage schedule (Table 1 generalised).  Items are (cycle, slice) pairs in flat
+// order p = K*N_S + j.  At stage k of a rank: receive item k; worker w processes
+// item k-2-2w and finalises (bins) item k-3-2w; the last worker hands item
+// k-1-2W to the ring successor.  Worker w of rank g in cycle K computes timestep
+// K*N_w + g*W + w, or passes the slice through unchanged when that timestep is
+// beyond the requested count (Q15).
+// ------------------------------------------------------------------------------
+enum OpKind { OP_RECV = 0, OP_FORCE, OP_PASS, OP_BIN, OP_SEND };
+
+struct Op {
+    int kind;
+    int stage;
+    int worker;
+    int slice;
+    int cycle;
+    int64_t t_rel;  // timestep relative to the start of the call (FORCE only)
+};
+
+struct Plan {
+    std::vector<Op> ops;
+    int n_stages = 0;
+};
+
+Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps)
+{
+    Plan P;
+    const int64_t nw = (int64_t)ng * W;
+    const int64_t n_cycles = n_steps <= 0 ? 0 : (n_steps + nw - 1) / nw;
+    const int64_t items = n_cycles * ns;
+    if (items == 0) return P;
+    auto active = [&](int64_t K, int w) { return K * nw + (int64_t)rank * W + w < n_steps; };
+    // receive set
+    int64_t r_lo = 0, r_hi = 0;  // items received at stage == item index
+    if (ng > 1) {
+        if (rank == 0) { r_lo = ns; r_hi = items + ns; }
+        else { r_lo = 0; r_hi = items; }
+    }
+    const int64_t last_compute = items - 1 + 3 + 2 * (int64_t)(W - 1);
+    const int64_t last_stage = std::max<int64_t>(last_compute, r_hi - 1);
+    for (int64_t k = 0; k <= last_stage; k++) {
+        if (k >= r_lo && k < r_hi) {
+            P.ops.push_back({OP_RECV, (int)k, -1, (int)(k % ns), (int)(k / ns), -1});
+        }
+        for (int w = 0; w < W; w++) {
+            const int64_t p = k - 2 - 2 * (int64_t)w;
+            if (p >= 0 && p < items) {
+                const int64_t K = p / ns;
+                const int j = (int)(p % ns);
+                if (active(K, w))
+                    P.ops.push_back({OP_FORCE, (int)k, w, j, (int)K, K * nw + (int64_t)rank * W + w});
+                else
+                    P.ops.push_back({OP_PASS, (int)k, w, j, (int)K, -1});
+            }
+            const int64_t q = k - 3 - 2 * (int64_t)w;
+            if (q >= 0 && q < items) {
+                const int64_t K = q / ns;
+                const int m = (int)(q % ns);
+                if (active(K, w)) P.ops.push_back({OP_BIN, (int)k, w, m, (int)K, -1});
+                if (w == W - 1) P.ops.push_back({OP_SEND, (int)k, w, m, (int)K, -1});
+            }
+        }
+    }
+    P.n_stages = (int)(last_stage + 1);
+    return P;
+}
+}  // namespace
+
+// ------------------------------------------------------------------------------
+// Context
+// ------------------------------------------------------------------------------
+struct dsea_ctx {
+    dsea_box_params box{};
+    double a = 0, b[3] = {0, 0, 0};
+    int64_t N = 0;
+    std::vector<double> h_xyz, h_v, h_f;  // host state by id (before dsea_slice)
+
+    bool sliced = false;
+    dsea_slice_params sp{};
+    dsea_geometry geo{};
+    Geo g{};
+    Tiling T{};
+    SlotLayout L{};
+    int mode = DSEA_MODE_FUSED;
+    int W = 1, NG = 1, rank = 0, device = 0;
+
+    cudaStream_t cs = nullptr, ss = nullptr, rs = nullptr;
+    BufView inb{};
+    std::vector<BufView> outb;
+    std::vector<StgView> stg;
+    std::vector<void*> dallocs;
+    UnitEnergy* e_dev = nullptr;
+    size_t e_cap = 0;
+    double4* partials = nullptr;
+    unsigned* tickets = nullptr;
+    DevErr* err_dev = nullptr;
+    std::vector<cudaEvent_t> ev_recv, ev_free, ev_bin, ev_send;
+
+    bool connected = false;
+    ncclComm_t send_comm = nullptr, recv_comm = nullptr;
+
+    // host mirror of the device state (rank 0), valid until the next mutation
+    std::vector<char> mirror;
+    bool mirror_valid = false;
+    bool holds_state = false;
+
+    std::vector<dsea_energy> energies;
+    int64_t steps_done = 0;
+
+    bool timing = false;
+    std::vector<cudaEvent_t> tev_pool;
+    size_t tev_used = 0;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tpairs;  // kind, (start, stop)
+    dsea_stats stats{};
+
+    std::string msg;
+};
+
+namespace {
+dsea_status fail(dsea_ctx* c, dsea_status s, const char* fmt, ...)
+{
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->msg = buf;
+    }
+    return s;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                   \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return fail(ctx, _e == cudaErrorMemoryAllocation ? DSEA_ENOMEM : DSEA_ECUDA,      \
+                        "%s: %s", #expr, cudaGetErrorString(_e));                            \
+    } while (0)
+
+// Geometry (§4) with the slicing of P:63-73 §3 and reading Q3.
+dsea_status compute_geometry(const dsea_box_params* box, const dsea_slice_params* sp,
+                             dsea_geometry* out, std::string* why)
+{
+    std::memset(out, 0, sizeof *out);
+    const int c = sp->cells_per_slice_x;
+    const double a = std::cbrt(4.0 / box->rho);
+    out->a = a;
+    out->b[0] = box->nx * a;
+    out->b[1] = box->ny * a;
+    out->b[2] = box->nz * a;
+    out->n_atoms = 4LL * box->nx * box->ny * box->nz;
+    const double sr6 = 1.0 / (box->rc * box->rc * box->rc * box->rc * box->rc * box->rc);
+    out->u_shift = sr6 - sr6 * sr6;
+    if (c < 1) { *why = "cells_per_slice_x must be >= 1"; return DSEA_EINVAL; }
+    int ns = sp->n_slices > 0 ? sp->n_slices : (int)std::floor(out->b[0] / (c * box->rc));
+    out->n_slices = ns;
+    out->cells[0] = c * ns;
+    out->cells[1] = (int)std::floor(out->b[1] / box->rc);
+    out->cells[2] = (int)std::floor(out->b[2] / box->rc);
+    for (int d = 0; d < 3; d++) out->l[d] = out->cells[d] > 0 ? out->b[d] / out->cells[d] : 0.0;
+    out->w = ns > 0 ? out->b[0] / ns : 0.0;
+    const int W = sp->workers_per_gpu > 0 ? sp->workers_per_gpu : 1;
+    out->n_max = ns / (2 + W * 2);
+    const double cf = sp->capacity_factor > 0 ? sp->capacity_factor : 1.25;
+    const double mean = ns > 0 ? (double)out->n_atoms / ns : 0.0;
+    long long cap = (long long)std::ceil(cf * mean + 4.0 * std::sqrt(mean) + 8.0);
+    cap = (cap + 31) / 32 * 32;
+    out->slot_capacity = (int)std::min<long long>(cap, 1LL << 30);
+    char buf[256];
+    if (ns < 1) { *why = "slice width: b_x < c*rc gives no slice"; return DSEA_EGEOM; }
+    if (out->cells[1] < 3 || out->cells[2] < 3) {
+        snprintf(buf, sizeof buf, "need >= 3 cells in y and z (got %d x %d); b_y, b_z >= 3 rc",
+                 out->cells[1], out->cells[2]);
+        *why = buf;
+        return DSEA_EGEOM;
+    }
+    if (out->l[0] < box->rc || out->l[1] < box->rc || out->l[2] < box->rc) {
+        snprintf(buf, sizeof buf, "cell edge below rc: l = (%.6g, %.6g, %.6g), rc = %.6g "
+                 "(slice width %.6g with %d cells per slice)", out->l[0], out->l[1], out->l[2],
+                 box->rc, out->w, c);
+        *why = buf;
+        return DSEA_EGEOM;
+    }
+    return DSEA_OK;
+}
+
+// FCC lattice, offset a/4 (Q10); id = ((ix*ny + iy)*nz + iz)*4 + k.
+void host_lattice(const dsea_box_params& bx, double a, double* xyz)
+{
+    const double basis[4][3] = {{0.0, 0.0, 0.0}, {0.5, 0.5, 0.0}, {0.5, 0.0, 0.5}, {0.0, 0.5, 0.5}};
+    int64_t id = 0;
+    for (int ix = 0; ix < bx.nx; ix++)
+        for (int iy = 0; iy < bx.ny; iy++)
+            for (int iz = 0; iz < bx.nz; iz++)
+                for (int k = 0; k < 4; k++, id++) {
+                    xyz[3 * id + 0] = (ix + basis[k][0] + 0.25) * a;
+                    xyz[3 * id + 1] = (iy + basis[k][1] + 0.25) * a;
+                    xyz[3 * id + 2] = (iz + basis[k][2] + 0.25) * a;
+                }
+}
+
+// Velocities "initialized according to the temperature", reading Q9:
+// splitmix64 stream -> 53-bit uniforms -> Box-Muller cosine branch, drawn in id
+// order x, y, z; zero momentum; exact rescale to T0 with 3N degrees of freedom.
+struct SplitMix {
+    uint64_t s;
+    uint64_t next()
+    {
+        s += 0x9E3779B97F4A7C15ULL;
+        uint64_t z = s;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    }
+    double uniform() { return (double)(next() >> 11) * (1.0 / 9007199254740992.0); }
+};
+
+void host_velocities(int64_t n, uint64_t seed, double T0, double* v)
+{
+    SplitMix rng{seed};
+    for (int64_t i = 0; i < 3 * n; i++) {
+        const double u1 = rng.uniform();
+        const double u2 = rng.uniform();
+        v[i] = std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(2.0 * 3.141592653589793 * u2);
+    }
+    for (int d = 0; d < 3; d++) {
+        double s = 0.0;
+        for (int64_t i = 0; i < n; i++) s += v[3 * i + d];
+        const double mean = s / (double)n;
+        for (int64_t i = 0; i < n; i++) v[3 * i + d] -= mean;
+    }
+    double s2 = 0.0;
+    for (int64_t i = 0; i < n; i++)
+        s2 += v[3 * i] * v[3 * i] + v[3 * i + 1] * v[3 * i + 1] + v[3 * i + 2] * v[3 * i + 2];
+    const double f = std::sqrt(T0 / (s2 / (3.0 * (double)n)));
+    for (int64_t i = 0; i < 3 * n; i++) v[i] *= f;
+}
+
+void free_device(dsea_ctx* c)
+{
+    if (c->sliced) cudaSetDevice(c->device);
+    if (c->connected) {
+        if (nccl().ok) {
+            if (c->send_comm) nccl().CommDestroy(c->send_comm);
+            if (c->recv_comm) nccl().CommDestroy(c->recv_comm);
+        }
+        c->send_comm = c->recv_comm = nullptr;
+        c->connected = false;
+    }
+    for (void* p : c->dallocs) cudaFree(p);
+    c->dallocs.clear();
+    for (auto* v : {&c->ev_recv, &c->ev_free, &c->ev_bin, &c->ev_send})
+        for (cudaEvent_t e : *v) cudaEventDestroy(e);
+    c->ev_recv.clear(); c->ev_free.clear(); c->ev_bin.clear(); c->ev_send.clear();
+    for (cudaEvent_t e : c->tev_pool) cudaEventDestroy(e);
+    c->tev_pool.clear();
+    c->tpairs.clear();
+    c->tev_used = 0;
+    if (c->cs) cudaStreamDestroy(c->cs);
+    if (c->ss) cudaStreamDestroy(c->ss);
+    if (c->rs) cudaStreamDestroy(c->rs);
+    c->cs = c->ss = c->rs = nullptr;
+    c->e_dev = nullptr; c->e_cap = 0;
+    c->outb.clear(); c->stg.clear();
+    c->sliced = false;
+    c->holds_state = false;
+    c->mirror_valid = false;
+}
+
+template <class T>
+dsea_status dalloc(dsea_ctx* c, T** p, size_t count)
+{
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, std::max<size_t>(count * sizeof(T), 256));
+    if (e != cudaSuccess)
+        return fail(c, DSEA_ENOMEM, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+    c->dallocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return DSEA_OK;
+}
+
+dsea_status alloc_buf(dsea_ctx* c, BufView* B)
+{
+    dsea_status s;
+    B->L = c->L;
+    if ((s = dalloc(c, &B->base, c->L.slot_bytes * (size_t)c->g.ns))) return s;
+    if ((s = dalloc(c, &B->cnt, (size_t)c->g.ns * c->g.ncell))) return s;
+    if ((s = dalloc(c, &B->perm, (size_t)c->g.ns * c->g.cap))) return s;
+    CUDA_TRY(c, cudaMemset(B->cnt, 0, sizeof(int32_t) * (size_t)c->g.ns * c->g.ncell));
+    CUDA_TRY(c, cudaMemset(B->base, 0, c->L.slot_bytes * (size_t)c->g.ns));
+    return DSEA_OK;
+}
+
+dsea_status alloc_stg(dsea_ctx* c, StgView* S)
+{
+    dsea_status s;
+    const size_t n = (size_t)c->g.ns * c->g.cap;
+    double** d[] = {&S->x, &S->y, &S->z, &S->vx, &S->vy, &S->vz, &S->fx, &S->fy, &S->fz};
+    for (auto* p : d)
+        if ((s = dalloc(c, p, n))) return s;
+    if ((s = dalloc(c, &S->id, n))) return s;
+    if ((s = dalloc(c, &S->key, n))) return s;
+    if ((s = dalloc(c, &S->n, (size_t)c->g.ns))) return s;
+    return DSEA_OK;
+}
+
+dsea_status check_dev_err(dsea_ctx* c)
+{
+    DevErr e{};
+    CUDA_TRY(c, cudaMemcpy(&e, c->err_dev, sizeof e, cudaMemcpyDeviceToHost));
+    if (e.code == 0) return DSEA_OK;
+    CUDA_TRY(c, cudaMemset(c->err_dev, 0, sizeof(DevErr)));
+    switch (e.code) {
+    case DSEA_ECAPACITY:
+        return fail(c, DSEA_ECAPACITY, "capacity exceeded: slice %d needs %d (slot capacity %d, "
+                    "force-tile staging capacity %d)", e.slice, e.aux, c->g.cap, c->T.smax);
+    case DSEA_EUNSTABLE:
+        return fail(c, DSEA_EUNSTABLE, "atom %d left slice %d for slice %d in one step (or became "
+                    "non-finite): timestep too large", e.atom, e.slice, e.aux);
+    case DSEA_EINVAL:
+        return fail(c, DSEA_EINVAL, "atom %d lies outside [0,b_x] x [0,b_y) x [0,b_z)", e.atom);
+    default:
+        return fail(c, (dsea_status)e.code, "device error %d", e.code);
+    }
+}
+
+// Bin the flat host state (by id) into the slots of the input buffer.
+dsea_status upload_state(dsea_ctx* c, const double* xyz, const double* v, const double* f)
+{
+    const int64_t N = c->N;
+    std::vector<double> soa((size_t)N * 9);
+    std::vector<int32_t> ids((size_t)N);
+    for (int64_t i = 0; i < N; i++) {
+        for (int d = 0; d < 3; d++) {
+            soa[(size_t)d * N + i] = xyz[3 * i + d];
+            soa[(size_t)(3 + d) * N + i] = v[3 * i + d];
+            soa[(size_t)(6 + d) * N + i] = f ? f[3 * i + d] : 0.0;
+        }
+        ids[(size_t)i] = (int32_t)i;
+    }
+    StgView& S = c->stg[0];
+    double* dst[] = {S.x, S.y, S.z, S.vx, S.vy, S.vz, S.fx, S.fy, S.fz};
+    for (int a = 0; a < 9; a++)
+        CUDA_TRY(c, cudaMemcpyAsync(dst[a], soa.data() + (size_t)a * N, sizeof(double) * N,
+                                    cudaMemcpyHostToDevice, c->cs));
+    CUDA_TRY(c, cudaMemcpyAsync(S.id, ids.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, c->cs));
+    init_keys_launch(c->g, S, (int)N, c->inb.cnt, c->err_dev, c->cs);
+    bin_scan_launch(c->g, c->inb, 0, c->g.ns, c->err_dev, c->cs);
+    bin_place_launch(c->g, c->inb, S, 0, 0, (int)N, 0, c->g.ns, c->err_dev, c->cs);
+    bin_gather_launch(c->g, c->inb, S, 0, c->g.ns, c->err_dev, c->cs);
+    c->stats.kernel_launches += 4;
+    CUDA_TRY(c, cudaStreamSynchronize(c->cs));
+    CUDA_TRY(c, cudaGetLastError());
+    dsea_status s = check_dev_err(c);
+    if (s) return s;
+    c->holds_state = true;
+    c->mirror_valid = false;
+    return DSEA_OK;
+}
+
+dsea_status fetch_mirror(dsea_ctx* c)
+{
+    if (c->mirror_valid) return DSEA_OK;
+    const size_t bytes = c->L.slot_bytes * (size_t)c->g.ns;
+    c->mirror.resize(bytes);
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemcpy(c->mirror.data(), c->inb.base, bytes, cudaMemcpyDeviceToHost));
+    c->mirror_valid = true;
+    return DSEA_OK;
+}
+
+// iterate atoms of the mirror: fn(slice, index_in_slot, cell_local, id, slot_base)
+template <class F>
+void for_each_atom(dsea_ctx* c, F fn)
+{
+    for (int j = 0; j < c->g.ns; j++) {
+        const char* base = c->mirror.data() + (size_t)j * c->L.slot_bytes;
+        const int32_t* cs = reinterpret_cast<const int32_t*>(base);
+        const int32_t* ids = reinterpret_cast<const int32_t*>(base + c->L.off_id);
+        for (int cell = 0; cell < c->g.ncell; cell++)
+            for (int i = cs[cell]; i < cs[cell + 1]; i++) fn(j, i, cell, ids[i], base);
+    }
+}
+
+dsea_status get_vec(dsea_ctx* c, double* out, int64_t n, int which)
+{
+    if (!c) return DSEA_EINVAL;
+    if (!out || n != c->N) return fail(c, DSEA_EINVAL, "array of %lld atoms expected", (long long)c->N);
+    if (!c->sliced) {
+        const std::vector<double>& src = which == 0 ? c->h_xyz : which == 1 ? c->h_v : c->h_f;
+        std::memcpy(out, src.data(), sizeof(double) * 3 * (size_t)c->N);
+        return DSEA_OK;
+    }
+    if (!c->holds_state) return fail(c, DSEA_ESTATE, "this rank does not hold the state (rank 0 does)");
+    dsea_status s = fetch_mirror(c);
+    if (s) return s;
+    const size_t off[3][3] = {{c->L.off_x, c->L.off_y, c->L.off_z},
+                              {c->L.off_vx, c->L.off_vy, c->L.off_vz},
+                              {c->L.off_fx, c->L.off_fy, c->L.off_fz}};
+    int64_t seen = 0;
+    for_each_atom(c, [&](int, int i, int, int id, const char* base) {
+        for (int d = 0; d < 3; d++)
+            out[3 * (int64_t)id + d] = reinterpret_cast<const double*>(base + off[which][d])[i];
+        seen++;
+    });
+    if (seen != c->N) return fail(c, DSEA_ESTATE, "slots hold %lld atoms, expected %lld", (long long)seen, (long long)c->N);
+    return DSEA_OK;
+}
+
+cudaEvent_t tev(dsea_ctx* c)
+{
+    if (c->tev_used == c->tev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->tev_pool.push_back(e);
+    }
+    return c->tev_pool[c->tev_used++];
+}
+
+enum { TK_FORCE = 0, TK_BIN = 1, TK_SEND = 2 };
+
+dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
+{
+    const int ns = c->g.ns;
+    const Plan P = build_plan(ns, c->NG, c->rank, c->W, n_steps);
+    std::vector<char> sent(ns, 0);
+    const size_t sb = c->L.slot_bytes;
+    NcclApi& api = nccl();
+    const int W = c->W;
+    auto in_of = [&](int w) -> BufView& { return w == 0 ? c->inb : c->outb[w - 1]; };
+    for (const Op& op : P.ops) {
+        switch (op.kind) {
+        case OP_RECV: {
+            char* dst = c->inb.base + (size_t)op.slice * sb;
+            CUDA_TRY(c, cudaStreamWaitEvent(c->rs, c->ev_free[op.slice], 0));
+            ncclResult_t r = api.Recv(dst, sb, ncclChar, 0, c->recv_comm, c->rs);
+            if (r != ncclSuccess) return fail(c, DSEA_EPEER, "ncclRecv: %s", api.GetErrorString(r));
+            CUDA_TRY(c, cudaEventRecord(c->ev_recv[op.slice], c->rs));
+            break;
+        }
+        case OP_FORCE: {
+            const int j = op.slice, w = op.worker;
+            if (w == 0 && c->NG > 1 && !(c->rank == 0 && op.cycle == 0)) {
+                const int need = std::min(j + 1, ns - 1);
+                CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[need], 0));
+            }
+            cudaEvent_t t0 = nullptr, t1 = nullptr;
+            if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
+            force_launch(c->g, c->T, in_of(w), c->stg[w], c->outb[w].cnt, j, 1,
+                         c->e_dev + (size_t)op.t_rel * ns, c->partials, c->tickets, c->err_dev, c->cs);
+            c->stats.kernel_launches++;
+            c->stats.force_launches++;
+            if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_FORCE, {t0, t1}}); }
+            if (w == 0 && c->NG > 1) {
+                if (j > 0) CUDA_TRY(c, cudaEventRecord(c->ev_free[j - 1], c->cs));
+                if (j == ns - 1) CUDA_TRY(c, cudaEventRecord(c->ev_free[j], c->cs));
+            }
+            break;
+        }
+        case OP_PASS: {
+            const int j = op.slice, w = op.worker;
+            if (w == 0 && c->NG > 1 && !(c->rank == 0 && op.cycle == 0))
+                CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[j], 0));
+            if (w == W - 1 && c->NG > 1 && sent[j]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[j], 0));
+            BufView& src = in_of(w);
+            BufView& dst = c->outb[w];
+            if (src.base != dst.base)
+                CUDA_TRY(c, cudaMemcpyAsync(dst.base + (size_t)j * sb, src.base + (size_t)j * sb, sb,
+                                            cudaMemcpyDeviceToDevice, c->cs));
+            if (w == 0 && c->NG > 1) CUDA_TRY(c, cudaEventRecord(c->ev_free[j], c->cs));
+            if (w == W - 1 && c->NG > 1) CUDA_TRY(c, cudaEventRecord(c->ev_bin[j], c->cs));
+            break;
+        }
+        case OP_BIN: {
+            const int m = op.slice, w = op.worker;
+            if (w == W - 1 && c->NG > 1 && sent[m]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[m], 0));
+            cudaEvent_t t0 = nullptr, t1 = nullptr;
+            if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
+            const int s0 = std::max(m - 1, 0), s1 = std::min(m + 1, ns - 1);
+            BufView& ob = c->outb[w];
+            bin_scan_launch(c->g, ob, m, 1, c->err_dev, c->cs);
+            bin_place_launch(c->g, ob, c->stg[w], s0, s1 - s0 + 1, 0, m, 1, c->err_dev, c->cs);
+            bin_gather_launch(c->g, ob, c->stg[w], m, 1, c->err_dev, c->cs);
+            c->stats.kernel_launches += 3;
+            if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_BIN, {t0, t1}}); }
+            if (w == W - 1 && c->NG > 1) CUDA_TRY(c, cudaEventRecord(c->ev_bin[m], c->cs));
+            break;
+        }
+        case OP_SEND: {
+            if (c->NG == 1) break;  // ring of one: the last worker wrote into the input buffer
+            const int m = op.slice;
+            CUDA_TRY(c, cudaStreamWaitEvent(c->ss, c->ev_bin[m], 0));
+            cudaEvent_t t0 = nullptr, t1 = nullptr;
+            if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->ss); }
+            ncclResult_t r = api.Send(c->outb[W - 1].base + (size_t)m * sb, sb, ncclChar, 1,
+                                      c->send_comm, c->ss);
+            if (r != ncclSuccess) return fail(c, DSEA_EPEER, "ncclSend: %s", api.GetErrorString(r));
+            if (c->timing) { cudaEventRecord(t1, c->ss); c->tpairs.push_back({TK_SEND, {t0, t1}}); }
+            CUDA_TRY(c, cudaEventRecord(c->ev_send[m], c->ss));
+            sent[m] = 1;
+            c->stats.hop_bytes += (int64_t)sb;
+            break;
+        }
+        }
+    }
+    return DSEA_OK;
+}
+
+dsea_status run_fused(dsea_ctx* c, int64_t n_steps)
+{
+    const int ns = c->g.ns;
+    for (int64_t t = 0; t < n_steps; t++) {
+        cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr;
+        if (c->timing) { t0 = tev(c); t1 = tev(c); t2 = tev(c); cudaEventRecord(t0, c->cs); }
+        force_launch(c->g, c->T, c->inb, c->stg[0], c->inb.cnt, 0, ns, c->e_dev + (size_t)t * ns,
+                     c->partials, c->tickets, c->err_dev, c->cs);
+        if (c->timing) cudaEventRecord(t1, c->cs);
+        bin_scan_launch(c->g, c->inb, 0, ns, c->err_dev, c->cs);
+        bin_place_launch(c->g, c->inb, c->stg[0], 0, ns, 0, 0, ns, c->err_dev, c->cs);
+        bin_gather_launch(c->g, c->inb, c->stg[0], 0, ns, c->err_dev, c->cs);
+        if (c->timing) {
+            cudaEventRecord(t2, c->cs);
+            c->tpairs.push_back({TK_FORCE, {t0, t1}});
+            c->tpairs.push_back({TK_BIN, {t1, t2}});
+        }
+        c->stats.kernel_launches += 4;
+        c->stats.force_launches += 1;
+    }
+    return DSEA_OK;
+}
+}  // namespace
+
+// ==============================================================================
+// C ABI
+// ==============================================================================
+extern "C" {
+
+dsea_status dsea_init(const dsea_box_params* box, dsea_ctx** out)
+{
+    if (!out) return DSEA_EINVAL;
+    *out = nullptr;
+    if (!box || box->nx < 1 || box->ny < 1 || box->nz < 1 || !(box->rho > 0) || !(box->rc > 0) ||
+        !(box->dt > 0) || !(box->T0 >= 0))
+        return DSEA_EINVAL;
+    const int64_t N = 4LL * box->nx * box->ny * box->nz;
+    if (N > (1LL << 30)) return DSEA_EINVAL;
+    dsea_ctx* c = new (std::nothrow) dsea_ctx();
+    if (!c) return DSEA_ENOMEM;
+    c->box = *box;
+    c->a = std::cbrt(4.0 / box->rho);
+    c->b[0] = box->nx * c->a;
+    c->b[1] = box->ny * c->a;
+    c->b[2] = box->nz * c->a;
+    c->N = N;
+    try {
+        c->h_xyz.resize((size_t)N * 3);
+        c->h_v.resize((size_t)N * 3);
+        c->h_f.assign((size_t)N * 3, 0.0);  // F_new = F_old = 0 at start (Q7)
+    } catch (...) {
+        delete c;
+        return DSEA_ENOMEM;
+    }
+    host_lattice(*box, c->a, c->h_xyz.data());
+    host_velocities(N, box->seed, box->T0, c->h_v.data());
+    *out = c;
+    return DSEA_OK;
+}
+
+dsea_status dsea_geometry_compute(const dsea_box_params* box, const dsea_slice_params* sp,
+                                  dsea_geometry* out)
+{
+    if (!box || !sp || !out || !(box->rho > 0) || !(box->rc > 0) || box->nx < 1 || box->ny < 1 ||
+        box->nz < 1)
+        return DSEA_EINVAL;
+    std::string why;
+    return compute_geometry(box, sp, out, &why);
+}
+
+dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
+{
+    if (!c) return DSEA_EINVAL;
+    if (!sp) return fail(c, DSEA_EINVAL, "null slice params");
+    if (sp->n_gpus < 1 || sp->rank < 0 || sp->rank >= sp->n_gpus || sp->workers_per_gpu < 1 ||
+        sp->device < 0 || sp->mode < 0 || sp->mode > 2)
+        return fail(c, DSEA_EINVAL, "bad slice params (n_gpus %d, rank %d, W %d, device %d, mode %d)",
+                    sp->n_gpus, sp->rank, sp->workers_per_gpu, sp->device, sp->mode);
+    int mode = sp->mode;
+    if (mode == DSEA_MODE_AUTO) mode = (sp->n_gpus == 1 && sp->workers_per_gpu == 1) ? DSEA_MODE_FUSED : DSEA_MODE_STAGED;
+    if (mode == DSEA_MODE_FUSED && (sp->n_gpus != 1 || sp->workers_per_gpu != 1))
+        return fail(c, DSEA_EINVAL, "fused mode needs n_gpus == 1 and workers_per_gpu == 1");
+    dsea_geometry geo;
+    std::string why;
+    dsea_status s = compute_geometry(&c->box, sp, &geo, &why);
+    if (s) return fail(c, s, "%s", why.c_str());
+    if (mode == DSEA_MODE_STAGED && sp->n_gpus == 1 && geo.n_slices < 2 + 2 * sp->workers_per_gpu)
+        return fail(c, DSEA_EGEOM, "a ring of one with W = %d workers needs N_S >= %d slices (Eq. 1), got %d",
+                    sp->workers_per_gpu, 2 + 2 * sp->workers_per_gpu, geo.n_slices);
+
+    // keep the current state (host mirror of the device or the host arrays)
+    std::vector<double> xyz, v, f;
+    if (c->sliced && c->holds_state) {
+        xyz.resize((size_t)c->N * 3); v.resize((size_t)c->N * 3); f.resize((size_t)c->N * 3);
+        if ((s = get_vec(c, xyz.data(), c->N, 0)) || (s = get_vec(c, v.data(), c->N, 1)) ||
+            (s = get_vec(c, f.data(), c->N, 2)))
+            return s;
+    } else if (!c->sliced) {
+        xyz = c->h_xyz; v = c->h_v; f = c->h_f;
+    }
+    free_device(c);
+
+    c->sp = *sp;
+    c->mode = mode;
+    c->geo = geo;
+    c->W = sp->workers_per_gpu;
+    c->NG = sp->n_gpus;
+    c->rank = sp->rank;
+    c->device = sp->device;
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(c, DSEA_ECUDA, "no CUDA device available (the engine has no CPU fallback)");
+    if (sp->device >= ndev) return fail(c, DSEA_EINVAL, "device %d of %d", sp->device, ndev);
+    CUDA_TRY(c, cudaSetDevice(sp->device));
+
+    Geo& g = c->g;
+    for (int d = 0; d < 3; d++) { g.b[d] = geo.b[d]; g.l[d] = geo.l[d]; g.cells[d] = geo.cells[d]; }
+    g.rc = c->box.rc;
+    g.rc2 = c->box.rc * c->box.rc;
+    g.dt = c->box.dt;
+    g.ushift = geo.u_shift;
+    g.c = sp->cells_per_slice_x;
+    g.ns = geo.n_slices;
+    g.ncell = g.c * geo.cells[1] * geo.cells[2];
+    g.cap = geo.slot_capacity;
+    g.rc2_screen = (float)(g.rc2 * (1.0 + 1e-5) + 1e-3);
+    c->L = make_slot_layout(g.ncell, g.cap);
+
+    int optin = 0;
+    CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, sp->device));
+    const double mean_per_cell = (double)c->N / ((double)g.ns * g.ncell);
+    c->T = choose_tiling(g, mean_per_cell, optin);
+    if (force_kernel_attr(c->T) != 0)
+        return fail(c, DSEA_ECUDA, "cannot set %zu bytes of dynamic shared memory", c->T.smem);
+
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->ss, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->rs, cudaStreamNonBlocking));
+    c->sliced = true;
+
+    // buffers: input buffer + one output buffer per worker; the last worker of a ring
+    // of one writes straight back into the input buffer (local hand-off).
+    if ((s = alloc_buf(c, &c->inb))) return s;
+    c->outb.resize(c->W);
+    for (int w = 0; w < c->W; w++) {
+        const bool alias = (w == c->W - 1) && c->NG == 1;
+        if (alias) c->outb[w] = c->inb;
+        else if ((s = alloc_buf(c, &c->outb[w]))) return s;
+    }
+    c->stg.resize(c->W);
+    for (int w = 0; w < c->W; w++)
+        if ((s = alloc_stg(c, &c->stg[w]))) return s;
+    if ((s = dalloc(c, &c->partials, (size_t)g.ns * c->T.tiles))) return s;
+    if ((s = dalloc(c, &c->tickets, (size_t)g.ns))) return s;
+    CUDA_TRY(c, cudaMemset(c->tickets, 0, sizeof(unsigned) * g.ns));
+    if ((s = dalloc(c, &c->err_dev, 1))) return s;
+    CUDA_TRY(c, cudaMemset(c->err_dev, 0, sizeof(DevErr)));
+    for (auto* v : {&c->ev_recv, &c->ev_free, &c->ev_bin, &c->ev_send}) {
+        v->resize(g.ns);
+        for (int j = 0; j < g.ns; j++) CUDA_TRY(c, cudaEventCreateWithFlags(&(*v)[j], cudaEventDisableTiming));
+    }
+
+    c->msg.clear();
+    if (c->NG > geo.n_max)
+        c->msg = "note: N_GPU exceeds N_max of Eq. (1); the ring runs at the plateau (P:364)";
+    if (c->rank == 0 || c->NG == 1) {
+        if (xyz.empty()) return fail(c, DSEA_ESTATE, "no state to slice");
+        if ((s = upload_state(c, xyz.data(), v.data(), f.data()))) return s;
+    }
+    return DSEA_OK;
+}
+
+dsea_status dsea_ring_unique_id(void* out, size_t out_bytes)
+{
+    if (!out || out_bytes < sizeof(ncclUniqueId)) return DSEA_EINVAL;
+    NcclApi& api = nccl();
+    if (!api.ok) return DSEA_EPEER;
+    ncclUniqueId id;
+    if (api.GetUniqueId(&id) != ncclSuccess) return DSEA_EPEER;
+    std::memcpy(out, &id, sizeof id);
+    return DSEA_OK;
+}
+
+dsea_status dsea_ring_connect(dsea_ctx* c, const void* ids, int32_t n_ids)
+{
+    if (!c) return DSEA_EINVAL;
+    if (!c->sliced) return fail(c, DSEA_ESTATE, "dsea_ring_connect before dsea_slice");
+    if (c->NG == 1) return DSEA_OK;
+    if (!ids || n_ids != c->NG) return fail(c, DSEA_EINVAL, "need %d link ids, got %d", c->NG, n_ids);
+    NcclApi& api = nccl();
+    if (!api.ok) return fail(c, DSEA_EPEER, "libnccl.so.2 not loadable");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    const ncclUniqueId* u = static_cast<const ncclUniqueId*>(ids);
+    const int prev = (c->rank - 1 + c->NG) % c->NG;
+    api.GroupStart();
+    ncclResult_t r1 = api.CommInitRank(&c->send_comm, 2, u[c->rank], 0);  // link rank -> rank+1
+    ncclResult_t r2 = api.CommInitRank(&c->recv_comm, 2, u[prev], 1);     // link prev -> rank
+    ncclResult_t r3 = api.GroupEnd();
+    if (r1 != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess)
+        return fail(c, DSEA_EPEER, "ncclCommInitRank: %s / %s / %s", api.GetErrorString(r1),
+                    api.GetErrorString(r2), api.GetErrorString(r3));
+    c->connected = true;
+    return DSEA_OK;
+}
+
+dsea_status dsea_step(dsea_ctx* c, int64_t n_steps)
+{
+    if (!c) return DSEA_EINVAL;
+    if (n_steps < 0) return fail(c, DSEA_EINVAL, "n_steps < 0");
+    if (!c->sliced) return fail(c, DSEA_ESTATE, "dsea_step before dsea_slice");
+    if (c->NG > 1 && !c->connected) return fail(c, DSEA_ESTATE, "ring not connected (dsea_ring_connect)");
+    if (n_steps == 0) return DSEA_OK;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    const int ns = c->g.ns;
+    const int64_t nw = (int64_t)c->NG * c->W;
+    const int64_t rows = ((n_steps + nw - 1) / nw) * nw;
+    if ((size_t)rows * ns > c->e_cap) {
+        if (c->e_dev) {
+            cudaFree(c->e_dev);
+            c->dallocs.erase(std::remove(c->dallocs.begin(), c->dallocs.end(), (void*)c->e_dev), c->dallocs.end());
+            c->e_dev = nullptr;
+        }
+        dsea_status s = dalloc(c, &c->e_dev, (size_t)rows * ns);
+        if (s) return s;
+        c->e_cap = (size_t)rows * ns;
+    }
+    c->mirror_valid = false;
+    c->tev_used = 0;
+    c->tpairs.clear();
+    dsea_status s = c->mode == DSEA_MODE_FUSED ? run_fused(c, n_steps) : run_plan(c, n_steps);
+    if (s) return s;
+    CUDA_TRY(c, cudaStreamSynchronize(c->cs));
+    CUDA_TRY(c, cudaStreamSynchronize(c->ss));
+    CUDA_TRY(c, cudaStreamSynchronize(c->rs));
+    CUDA_TRY(c, cudaGetLastError());
+    if ((s = check_dev_err(c))) return s;
+
+    // timing
+    for (auto& tp : c->tpairs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tp.second.first, tp.second.second);
+        if (tp.first == TK_FORCE) c->stats.force_ms += ms;
+        else if (tp.first == TK_BIN) c->stats.bin_ms += ms;
+        else c->stats.hop_ms += ms;
+    }
+    c->tpairs.clear();
+
+    // energies of the timesteps this rank computed, summed over slices in slice order
+    std::vector<UnitEnergy> he((size_t)rows * ns);
+    CUDA_TRY(c, cudaMemcpy(he.data(), c->e_dev, sizeof(UnitEnergy) * he.size(), cudaMemcpyDeviceToHost));
+    double last_pairs = 0;
+    for (int64_t t = 0; t < n_steps; t++) {
+        const int64_t owner_g = (t % nw) / c->W;
+        if (c->mode == DSEA_MODE_STAGED && owner_g != c->rank) continue;
+        double uc = 0, v2 = 0, k2 = 0, np = 0;
+        for (int j = 0; j < ns; j++) {
+            const UnitEnergy& e = he[(size_t)t * ns + j];
+            uc += e.u_core; v2 += e.vir2; k2 += e.ke2; np += e.npairs;
+        }
+        dsea_energy r;
+        r.step = c->steps_done + t;
+        r.U = 2.0 * uc + 2.0 * c->g.ushift * np;
+        r.V = 0.5 * v2;
+        r.KE = 0.5 * k2;
+        c->energies.push_back(r);
+        c->stats.atom_steps += c->N;
+        last_pairs = np;
+    }
+    c->stats.force_pairs = (int64_t)last_pairs;
+    c->steps_done += n_steps;
+    c->holds_state = (c->rank == 0);
+    return DSEA_OK;
+}
+
+void dsea_destroy(dsea_ctx* c)
+{
+    if (!c) return;
+    free_device(c);
+    delete c;
+}
+
+const char* dsea_last_error(const dsea_ctx* c)
+{
+    if (!c) return "null context";
+    return c->msg.c_str();
+}
+
+dsea_status dsea_get_geometry(const dsea_ctx* c, dsea_geometry* out)
+{
+    if (!c || !out) return DSEA_EINVAL;
+    if (!c->sliced) return DSEA_ESTATE;
+    *out = c->geo;
+    return DSEA_OK;
+}
+
+dsea_status dsea_get_positions(dsea_ctx* c, double* xyz, int64_t n) { return get_vec(c, xyz, n, 0); }
+dsea_status dsea_get_velocities(dsea_ctx* c, double* v, int64_t n) { return get_vec(c, v, n, 1); }
+dsea_status dsea_get_forces(dsea_ctx* c, double* f, int64_t n) { return get_vec(c, f, n, 2); }
+
+dsea_status dsea_get_cells(dsea_ctx* c, int32_t* cell_xyz, int32_t* slice, int64_t n)
+{
+    if (!c) return DSEA_EINVAL;
+    if (!cell_xyz || !slice || n != c->N) return fail(c, DSEA_EINVAL, "array of %lld atoms expected", (long long)c->N);
+    if (!c->sliced) return fail(c, DSEA_ESTATE, "dsea_get_cells before dsea_slice");
+    if (!c->holds_state) return fail(c, DSEA_ESTATE, "this rank does not hold the state (rank 0 does)");
+    dsea_status s = fetch_mirror(c);
+    if (s) return s;
+    const int CY = c->g.cells[1], CZ = c->g.cells[2];
+    for_each_atom(c, [&](int j, int, int cell, int id, const char*) {
+        const int cxl = cell / (CY * CZ);
+        cell_xyz[3 * (int64_t)id + 0] = j * c->g.c + cxl;
+        cell_xyz[3 * (int64_t)id + 1] = (cell / CZ) % CY;
+        cell_xyz[3 * (int64_t)id + 2] = cell % CZ;
+        slice[id] = j;
+    });
+    return DSEA_OK;
+}
+
+dsea_status dsea_get_energies(dsea_ctx* c, dsea_energy* out, int64_t cap, int64_t* n_written)
+{
+    if (!c || !n_written) return DSEA_EINVAL;
+    const int64_t n = std::min<int64_t>(cap, (int64_t)c->energies.size());
+    if (n > 0 && !out) return fail(c, DSEA_EINVAL, "null output");
+    for (int64_t i = 0; i < n; i++) out[i] = c->energies[(size_t)i];
+    *n_written = n < 0 ? 0 : n;
+    return DSEA_OK;
+}
+
+dsea_status dsea_set_state(dsea_ctx* c, const double* xyz, const double* v, const double* f, int64_t n)
+{
+    if (!c) return DSEA_EINVAL;
+    if (!xyz || !v || n != c->N) return fail(c, DSEA_EINVAL, "positions and velocities of %lld atoms expected", (long long)c->N);
+    if (!c->sliced) {
+        std::memcpy(c->h_xyz.data(), xyz, sizeof(double) * 3 * n);
+        std::memcpy(c->h_v.data(), v, sizeof(double) * 3 * n);
+        if (f) std::memcpy(c->h_f.data(), f, sizeof(double) * 3 * n);
+        else std::fill(c->h_f.begin(), c->h_f.end(), 0.0);
+        return DSEA_OK;
+    }
+    if (c->NG > 1 && c->rank != 0) return DSEA_OK;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    return upload_state(c, xyz, v, f);
+}
+
+dsea_status dsea_set_timing(dsea_ctx* c, int32_t enable)
+{
+    if (!c) return DSEA_EINVAL;
+    c->timing = enable != 0;
+    return DSEA_OK;
+}
+
+dsea_status dsea_get_stats(dsea_ctx* c, dsea_stats* out)
+{
+    if (!c || !out) return DSEA_EINVAL;
+    *out = c->stats;
+    return DSEA_OK;
+}
+
+dsea_status dsea_reset_stats(dsea_ctx* c)
+{
+    if (!c) return DSEA_EINVAL;
+    std::memset(&c->stats, 0, sizeof c->stats);
+    return DSEA_OK;
+}
+
+dsea_status dsea_schedule(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_t W, int32_t n_cycles,
+                          int32_t* rows, int64_t cap_rows, int64_t* n_rows)
+{
+    if (!n_rows || n_slices < 1 || n_gpus < 1 || rank < 0 || rank >= n_gpus || W < 1 || n_cycles < 0)
+        return DSEA_EINVAL;
+    const int64_t n_steps = (int64_t)n_cycles * n_gpus * W;
+    const Plan P = build_plan(n_slices, n_gpus, rank, W, n_steps);
+    // one row per (stage, worker) doing something; recv rows carry worker -1
+    std::vector<std::array<int32_t, 8>> out;
+    auto row_for = [&](int stage, int worker) -> std::array<int32_t, 8>& {
+        for (auto& r : out)
+            if (r[0] == stage && r[2] == worker) return r;
+        out.push_back({stage, -1, worker, -1, -1, -1, -1, -1});
+        return out.back();
+    };
+    for (const Op& op : P.ops) {
+        const int st = op.stage + 1;  // 1-based like Table 1
+        switch (op.kind) {
+        case OP_RECV: row_for(st, -1)[1] = op.slice + 1; row_for(st, -1)[6] = op.cycle; break;
+        case OP_FORCE:
+        case OP_PASS: {
+            auto& r = row_for(st, op.worker);
+            r[3] = op.slice + 1; r[6] = op.cycle; r[7] = op.kind == OP_FORCE ? (int32_t)op.t_rel : -1;
+            break;
+        }
+        case OP_BIN: row_for(st, op.worker)[4] = op.slice + 1; break;
+        case OP_SEND: row_for(st, op.worker)[5] = op.slice + 1; break;
+        }
+    }
+    if (n_gpus == 1) {
+        // single GPU: slices of the first super-cycle are loaded from storage at
+        // stages 1..N_S; show them as receives like Table 1
+        for (int j = 0; j < n_slices && n_cycles > 0; j++) {
+            auto& r = row_for(j + 1, -1);
+            r[1] = j + 1; r[6] = 0;
+        }
+    } else if (rank == 0) {
+        for (int j = 0; j < n_slices && n_cycles > 0; j++) {
+            auto& r = row_for(j + 1, -1);
+            if (r[1] < 0) { r[1] = j + 1; r[6] = 0; }
+        }
+    }
+    std::sort(out.begin(), out.end(), [](const std::array<int32_t, 8>& x, const std::array<int32_t, 8>& y) {
+        return x[0] != y[0] ? x[0] < y[0] : x[2] < y[2];
+    });
+    *n_rows = (int64_t)out.size();
+    if (rows) {
+        if (cap_rows < (int64_t)out.size()) return DSEA_EINVAL;
+        for (size_t i = 0; i < out.size(); i++)
+            for (int k = 0; k < 8; k++) rows[i * 8 + k] = out[i][k];
+    }
+    return DSEA_OK;
+}
+
+}  // extern "C"

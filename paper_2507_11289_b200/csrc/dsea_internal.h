@@ -1,0 +1,115 @@
+// dsea_internal.h -- layouts and kernel entry points shared by the host runtime
+// (dsea_host.cpp) and the sm_100a kernels (dsea_kernels.cu).  Not part of the ABI.
+//
+// HBM layout.  A *buffer* holds one slot per slice, slot j at
+// base + j*slot_bytes, each slot one contiguous block so that a ring hop is a
+// single transfer (§3.1):
+//   int32  cell_start[ncell+1]     cell prefix sums (CellNM = differences)
+//   double x[cap], y[cap], z[cap]  positions            (MolList, P:232-234,
+//   double vx[cap] vy[cap] vz[cap] velocities            redesigned as SoA,
+//   double fx[cap] fy[cap] fz[cap] F_new of the last pass  cell-sorted, padded)
+//   int32  id[cap]
+// Atoms are sorted by (cell, z, id); cells are ordered (cx_local, cy, cz) with z
+// fastest, so every (cx, cy) column is one contiguous, z-sorted run.
+// A *staging* buffer (per worker) has the same per-slice SoA arrays (no
+// cell_start) plus int32 key[cap] = destination global cell (slice*ncell + cell).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dsea {
+
+struct Geo {
+    double b[3];
+    double l[3];
+    double rc, rc2, dt, ushift;
+    int cells[3];   // global cells per axis (cells[0] = c * n_slices)
+    int c;          // cells per slice along x
+    int ns;         // n_slices
+    int ncell;      // cells per slice = c * cells[1] * cells[2]
+    int cap;        // atoms per slot
+    float rc2_screen;  // fp32 pre-screen radius^2 (rc^2 + margin)
+};
+
+struct SlotLayout {
+    size_t slot_bytes;
+    size_t off_x, off_y, off_z, off_vx, off_vy, off_vz, off_fx, off_fy, off_fz, off_id;
+};
+
+inline SlotLayout make_slot_layout(int ncell, int cap) {
+    SlotLayout L;
+    auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+    size_t o = al(sizeof(int32_t) * (size_t)(ncell + 1));
+    size_t dbl = al(sizeof(double) * (size_t)cap);
+    L.off_x = o; o += dbl;
+    L.off_y = o; o += dbl;
+    L.off_z = o; o += dbl;
+    L.off_vx = o; o += dbl;
+    L.off_vy = o; o += dbl;
+    L.off_vz = o; o += dbl;
+    L.off_fx = o; o += dbl;
+    L.off_fy = o; o += dbl;
+    L.off_fz = o; o += dbl;
+    L.off_id = o; o += al(sizeof(int32_t) * (size_t)cap);
+    L.slot_bytes = o;
+    return L;
+}
+
+// Device view of a slot buffer.
+struct BufView {
+    char* base;
+    SlotLayout L;
+    int32_t* cnt;    // [ns*ncell] per-cell arrival counters / cursors (not sent)
+    int32_t* perm;   // [ns*cap] bin scratch (not sent)
+};
+
+// Device view of a staging buffer (flat SoA over ns*cap entries).
+struct StgView {
+    double *x, *y, *z, *vx, *vy, *vz, *fx, *fy, *fz;
+    int32_t *id, *key;
+    int32_t* n;      // [ns] atoms staged per slice
+};
+
+// Force-kernel tiling (one CTA = one (cx_local, cy) column x tz cells of z).
+struct Tiling {
+    int tz;          // home cells per z-tile
+    int nzt;         // z-tiles per column
+    int tiles;       // tiles per slice = c * cells[1] * nzt
+    int smax;        // staged atoms capacity of one CTA
+    int jpar;        // candidate parity groups (lanes = 32/jpar atoms x jpar)
+    int maxh;        // per-lane hit-list capacity
+    size_t smem;     // dynamic shared memory bytes
+};
+
+// Energy record of one (slice, timestep) unit.
+struct UnitEnergy {
+    double u_core;   // sum over in-cutoff ordered pairs of s6*(s6-1), s6 = r^-6
+    double vir2;     // sum of s6*(2 s6 - 1)  (V = vir2 / 2)
+    double ke2;      // sum of v.v after the kick (KE = ke2 / 2)
+    double npairs;   // number of in-cutoff ordered pairs
+};
+
+// Error record written by kernels (first error wins).
+struct DevErr {
+    int32_t code;    // 0 or a dsea_status
+    int32_t slice;
+    int32_t atom;    // atom id or -1
+    int32_t aux;
+};
+
+// ---- kernel launchers (dsea_kernels.cu) ----------------------------------
+int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t* out_cnt,
+                 int j0, int nj, UnitEnergy* e_out, double4* partials, unsigned* tickets,
+                 DevErr* err, cudaStream_t s);
+void bin_scan_launch(const Geo& g, BufView out, int m0, int nm, DevErr* err, cudaStream_t s);
+void bin_place_launch(const Geo& g, BufView out, StgView stg, int s0, int nsrc, int flat_count,
+                      int m0, int nm, DevErr* err, cudaStream_t s);
+void bin_gather_launch(const Geo& g, BufView out, StgView stg, int m0, int nm, DevErr* err,
+                       cudaStream_t s);
+void init_keys_launch(const Geo& g, StgView stg, int n, int32_t* out_cnt, DevErr* err,
+                      cudaStream_t s);
+Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin);
+int force_kernel_attr(const Tiling& T);
+
+}  // namespace dsea

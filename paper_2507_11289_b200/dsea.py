@@ -1,0 +1,329 @@
+"""Thin ctypes binding of libdsea.so (include/dsea.h).  Argument marshalling only:
+every step of the hot path runs in the library's sm_100a kernels.  There is no
+CPU fallback -- if the library cannot be loaded, importing this module raises.
+
+Functions carry the C names (dsea_init, dsea_slice, ...); `Engine` is a small
+convenience wrapper over them used by the tests and bench.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdsea.so")
+
+# status codes (dsea.h)
+DSEA_OK = 0
+DSEA_EINVAL = -1
+DSEA_EGEOM = -2
+DSEA_ESTATE = -3
+DSEA_ECAPACITY = -4
+DSEA_EUNSTABLE = -5
+DSEA_ECUDA = -6
+DSEA_ENOMEM = -7
+DSEA_EPEER = -8
+STATUS_NAMES = {0: "DSEA_OK", -1: "DSEA_EINVAL", -2: "DSEA_EGEOM", -3: "DSEA_ESTATE",
+                -4: "DSEA_ECAPACITY", -5: "DSEA_EUNSTABLE", -6: "DSEA_ECUDA", -7: "DSEA_ENOMEM",
+                -8: "DSEA_EPEER"}
+
+DSEA_MODE_AUTO = 0
+DSEA_MODE_FUSED = 1
+DSEA_MODE_STAGED = 2
+
+NCCL_ID_BYTES = 128
+
+
+class dsea_box_params(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+                ("rho", ctypes.c_double), ("rc", ctypes.c_double), ("dt", ctypes.c_double),
+                ("T0", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
+class dsea_slice_params(ctypes.Structure):
+    _fields_ = [("n_slices", ctypes.c_int32), ("cells_per_slice_x", ctypes.c_int32),
+                ("n_gpus", ctypes.c_int32), ("rank", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("workers_per_gpu", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("capacity_factor", ctypes.c_double)]
+
+
+class dsea_geometry(ctypes.Structure):
+    _fields_ = [("b", ctypes.c_double * 3), ("l", ctypes.c_double * 3), ("w", ctypes.c_double),
+                ("a", ctypes.c_double), ("u_shift", ctypes.c_double), ("cells", ctypes.c_int32 * 3),
+                ("n_slices", ctypes.c_int32), ("n_max", ctypes.c_int32),
+                ("slot_capacity", ctypes.c_int32), ("n_atoms", ctypes.c_int64)]
+
+
+class dsea_energy(ctypes.Structure):
+    _fields_ = [("step", ctypes.c_int64), ("U", ctypes.c_double), ("KE", ctypes.c_double),
+                ("V", ctypes.c_double)]
+
+
+class dsea_stats(ctypes.Structure):
+    _fields_ = [("kernel_launches", ctypes.c_int64), ("force_launches", ctypes.c_int64),
+                ("atom_steps", ctypes.c_int64), ("force_ms", ctypes.c_double),
+                ("bin_ms", ctypes.c_double), ("hop_ms", ctypes.c_double),
+                ("hop_bytes", ctypes.c_int64), ("force_pairs", ctypes.c_int64)]
+
+
+_c = ctypes.c_void_p
+_st = ctypes.c_int
+_pd = ctypes.POINTER(ctypes.c_double)
+_pi32 = ctypes.POINTER(ctypes.c_int32)
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+
+# (name, restype, argtypes) -- every symbol declared in include/dsea.h
+SIGNATURES = [
+    ("dsea_init", _st, [ctypes.POINTER(dsea_box_params), ctypes.POINTER(_c)]),
+    ("dsea_slice", _st, [_c, ctypes.POINTER(dsea_slice_params)]),
+    ("dsea_ring_connect", _st, [_c, ctypes.c_void_p, ctypes.c_int32]),
+    ("dsea_ring_unique_id", _st, [ctypes.c_void_p, ctypes.c_size_t]),
+    ("dsea_step", _st, [_c, ctypes.c_int64]),
+    ("dsea_destroy", None, [_c]),
+    ("dsea_last_error", ctypes.c_char_p, [_c]),
+    ("dsea_get_geometry", _st, [_c, ctypes.POINTER(dsea_geometry)]),
+    ("dsea_get_positions", _st, [_c, _pd, ctypes.c_int64]),
+    ("dsea_get_velocities", _st, [_c, _pd, ctypes.c_int64]),
+    ("dsea_get_forces", _st, [_c, _pd, ctypes.c_int64]),
+    ("dsea_get_cells", _st, [_c, _pi32, _pi32, ctypes.c_int64]),
+    ("dsea_get_energies", _st, [_c, ctypes.POINTER(dsea_energy), ctypes.c_int64, _pi64]),
+    ("dsea_set_state", _st, [_c, _pd, _pd, _pd, ctypes.c_int64]),
+    ("dsea_set_timing", _st, [_c, ctypes.c_int32]),
+    ("dsea_get_stats", _st, [_c, ctypes.POINTER(dsea_stats)]),
+    ("dsea_reset_stats", _st, [_c]),
+    ("dsea_geometry_compute", _st, [ctypes.POINTER(dsea_box_params),
+                                    ctypes.POINTER(dsea_slice_params), ctypes.POINTER(dsea_geometry)]),
+    ("dsea_schedule", _st, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                            ctypes.c_int32, _pi32, ctypes.c_int64, _pi64]),
+]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2507_11289_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    for name, res, args in SIGNATURES:
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+class DseaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(ctx, st):
+    if st != 0:
+        msg = lib.dsea_last_error(ctx).decode() if ctx else ""
+        raise DseaError(st, msg)
+
+
+def _pd_of(a):
+    return a.ctypes.data_as(_pd)
+
+
+# ---- same-name functional layer ---------------------------------------------------
+def dsea_init(nx, ny, nz, rho, rc, dt=0.0018, T0=1.0, seed=11289):
+    box = dsea_box_params(nx, ny, nz, rho, rc, dt, T0, seed)
+    ctx = ctypes.c_void_p()
+    st = lib.dsea_init(ctypes.byref(box), ctypes.byref(ctx))
+    if st != 0:
+        raise DseaError(st, "dsea_init rejected the box parameters")
+    return ctx
+
+
+def dsea_slice(ctx, n_slices=0, cells_per_slice_x=1, n_gpus=1, rank=0, device=0,
+               workers_per_gpu=1, mode=DSEA_MODE_AUTO, capacity_factor=0.0):
+    sp = dsea_slice_params(n_slices, cells_per_slice_x, n_gpus, rank, device, workers_per_gpu,
+                           mode, capacity_factor)
+    _check(ctx, lib.dsea_slice(ctx, ctypes.byref(sp)))
+
+
+def dsea_ring_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+    st = lib.dsea_ring_unique_id(buf, NCCL_ID_BYTES)
+    if st != 0:
+        raise DseaError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def dsea_ring_connect(ctx, ids: bytes, n_ids: int):
+    buf = ctypes.create_string_buffer(ids, len(ids))
+    _check(ctx, lib.dsea_ring_connect(ctx, buf, n_ids))
+
+
+def dsea_step(ctx, n_steps: int):
+    _check(ctx, lib.dsea_step(ctx, int(n_steps)))
+
+
+def dsea_destroy(ctx):
+    lib.dsea_destroy(ctx)
+
+
+def dsea_last_error(ctx) -> str:
+    return lib.dsea_last_error(ctx).decode()
+
+
+def dsea_get_geometry(ctx) -> dsea_geometry:
+    g = dsea_geometry()
+    _check(ctx, lib.dsea_get_geometry(ctx, ctypes.byref(g)))
+    return g
+
+
+def _n_atoms(ctx):
+    return dsea_get_geometry(ctx).n_atoms
+
+
+def dsea_get_positions(ctx, n_atoms, out=None):
+    out = np.empty((n_atoms, 3)) if out is None else out
+    _check(ctx, lib.dsea_get_positions(ctx, _pd_of(out), n_atoms))
+    return out
+
+
+def dsea_get_velocities(ctx, n_atoms, out=None):
+    out = np.empty((n_atoms, 3)) if out is None else out
+    _check(ctx, lib.dsea_get_velocities(ctx, _pd_of(out), n_atoms))
+    return out
+
+
+def dsea_get_forces(ctx, n_atoms, out=None):
+    out = np.empty((n_atoms, 3)) if out is None else out
+    _check(ctx, lib.dsea_get_forces(ctx, _pd_of(out), n_atoms))
+    return out
+
+
+def dsea_get_cells(ctx, n_atoms):
+    cells = np.empty((n_atoms, 3), dtype=np.int32)
+    sl = np.empty(n_atoms, dtype=np.int32)
+    _check(ctx, lib.dsea_get_cells(ctx, cells.ctypes.data_as(_pi32), sl.ctypes.data_as(_pi32), n_atoms))
+    return cells, sl
+
+
+def dsea_get_energies(ctx, cap=1 << 22):
+    n = ctypes.c_int64()
+    _check(ctx, lib.dsea_get_energies(ctx, None, 0, ctypes.byref(n)))
+    buf = (dsea_energy * cap)()
+    _check(ctx, lib.dsea_get_energies(ctx, buf, cap, ctypes.byref(n)))
+    arr = np.zeros((n.value, 4))
+    steps = np.zeros(n.value, dtype=np.int64)
+    for i in range(n.value):
+        e = buf[i]
+        steps[i] = e.step
+        arr[i] = (e.U, e.KE, e.V, e.U + e.KE)
+    return steps, arr
+
+
+def dsea_set_state(ctx, xyz, vxyz, fxyz=None):
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+    vxyz = np.ascontiguousarray(vxyz, dtype=np.float64)
+    f = None if fxyz is None else np.ascontiguousarray(fxyz, dtype=np.float64)
+    _check(ctx, lib.dsea_set_state(ctx, _pd_of(xyz), _pd_of(vxyz), None if f is None else _pd_of(f),
+                                   xyz.shape[0]))
+
+
+def dsea_set_timing(ctx, enable: bool):
+    _check(ctx, lib.dsea_set_timing(ctx, 1 if enable else 0))
+
+
+def dsea_get_stats(ctx) -> dsea_stats:
+    s = dsea_stats()
+    _check(ctx, lib.dsea_get_stats(ctx, ctypes.byref(s)))
+    return s
+
+
+def dsea_reset_stats(ctx):
+    _check(ctx, lib.dsea_reset_stats(ctx))
+
+
+def dsea_geometry_compute(nx, ny, nz, rho, rc, n_slices=0, cells_per_slice_x=1, workers_per_gpu=1,
+                          capacity_factor=0.0):
+    box = dsea_box_params(nx, ny, nz, rho, rc, 0.0018, 1.0, 0)
+    sp = dsea_slice_params(n_slices, cells_per_slice_x, 1, 0, 0, workers_per_gpu, 0, capacity_factor)
+    g = dsea_geometry()
+    st = lib.dsea_geometry_compute(ctypes.byref(box), ctypes.byref(sp), ctypes.byref(g))
+    return st, g
+
+
+def dsea_schedule(n_slices, n_gpus, rank, workers_per_gpu, n_cycles):
+    n = ctypes.c_int64()
+    _check(None, lib.dsea_schedule(n_slices, n_gpus, rank, workers_per_gpu, n_cycles, None, 0,
+                                   ctypes.byref(n)))
+    rows = np.zeros((n.value, 8), dtype=np.int32)
+    _check(None, lib.dsea_schedule(n_slices, n_gpus, rank, workers_per_gpu, n_cycles,
+                                   rows.ctypes.data_as(_pi32), n.value, ctypes.byref(n)))
+    return rows
+
+
+# ---- convenience wrapper ----------------------------------------------------------
+@dataclass
+class Box:
+    nx: int
+    ny: int
+    nz: int
+    rho: float = 0.8
+    rc: float = 2.5
+    dt: float = 0.0018
+    T0: float = 1.0
+    seed: int = 11289
+
+
+class Engine:
+    """One context = one GPU.  For a ring, one Engine per process (rank)."""
+
+    def __init__(self, box: Box):
+        self.box = box
+        self.ctx = dsea_init(box.nx, box.ny, box.nz, box.rho, box.rc, box.dt, box.T0, box.seed)
+        self.n_atoms = 4 * box.nx * box.ny * box.nz
+
+    def slice(self, **kw):
+        dsea_slice(self.ctx, **kw)
+        return self
+
+    @property
+    def geometry(self):
+        return dsea_get_geometry(self.ctx)
+
+    def step(self, n):
+        dsea_step(self.ctx, n)
+
+    def positions(self):
+        return dsea_get_positions(self.ctx, self.n_atoms)
+
+    def velocities(self):
+        return dsea_get_velocities(self.ctx, self.n_atoms)
+
+    def forces(self):
+        return dsea_get_forces(self.ctx, self.n_atoms)
+
+    def cells(self):
+        return dsea_get_cells(self.ctx, self.n_atoms)
+
+    def energies(self):
+        return dsea_get_energies(self.ctx)
+
+    def set_state(self, xyz, v, f=None):
+        dsea_set_state(self.ctx, xyz, v, f)
+
+    def stats(self):
+        return dsea_get_stats(self.ctx)
+
+    def close(self):
+        if self.ctx:
+            dsea_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,252 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Tolerances from the north star (BASELINE.json) with readings
+Q13/Q14:
+  cells and slice membership ............ bit-exact (oracle binning of the GPU positions)
+  per-atom forces (fp64) ................ |dF| <= 1e-10 * max(|F_oracle|, F_rms)
+  positions after 10 steps .............. <= 1e-8 sigma (minimum image in y/z)
+  energy drift over 1000 NVE steps ...... |dE/E| < 1e-4
+Run on a B200 with -m gpu."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2507_11289_b200 import CONFIGS
+from paper_2507_11289_b200 import dsea as D
+from tests import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(cfg, seed=None, **kw):
+    c = CONFIGS[cfg] if isinstance(cfg, str) else cfg
+    e = D.Engine(D.Box(c.nx, c.ny, c.nz, c.rho, c.rc, c.dt, c.T0, c.seed if seed is None else seed))
+    kw.setdefault("n_slices", c.n_slices)
+    kw.setdefault("cells_per_slice_x", c.cells_per_slice_x)
+    e.slice(**kw)
+    return e, c
+
+
+def _geom(c):
+    return oracle.geometry(c.nx, c.ny, c.nz, c.rho, c.rc, c.n_slices, c.cells_per_slice_x)
+
+
+def _force_close(Fg, Fo, tol=1e-10):
+    frms = np.sqrt((Fo ** 2).sum(1).mean())
+    err = np.sqrt(((Fg - Fo) ** 2).sum(1))
+    ref = np.maximum(np.sqrt((Fo ** 2).sum(1)), frms)
+    worst = (err / ref).max()
+    assert worst <= tol, worst
+    return worst
+
+
+def _min_image(d, b):
+    d = d.copy()
+    d[:, 1:] -= b[1:] * np.round(d[:, 1:] / b[1:])
+    return d
+
+
+def _cells_exact(e, c):
+    g = _geom(c)
+    x = e.positions()
+    cg, sg = e.cells()
+    co, so = oracle.bin_atoms(x, g.l, g.cells, c.cells_per_slice_x)
+    assert np.array_equal(cg, co)
+    assert np.array_equal(sg, so)
+    counts = np.bincount(sg, minlength=g.n_slices)
+    assert counts.sum() == c.n_atoms
+
+
+@pytest.mark.parametrize("cfg", ["C1", "P8"])
+def test_initial_binning_bit_exact(cfg):
+    e, c = _engine(cfg)
+    x0 = oracle.lattice(c.nx, c.ny, c.nz, _geom(c).a)
+    assert np.array_equal(e.positions(), x0)
+    _cells_exact(e, c)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "P8"])
+def test_first_step_forces_energies_lattice(cfg):
+    """Step 0 from the lattice: F_new(r_0), U, V, KE against the oracle."""
+    e, c = _engine(cfg)
+    g = _geom(c)
+    x0 = e.positions()
+    v0 = e.velocities()
+    e.step(1)
+    xo, vo, Fo, eo = oracle.run(x0, v0, np.zeros_like(x0), g.b, c.rc, c.dt, 1)
+    _force_close(e.forces(), Fo)
+    steps, en = e.energies()
+    assert steps.tolist() == [0]
+    assert np.allclose(en[0, :3], eo[0, :3], rtol=1e-10, atol=1e-9)
+    assert np.max(np.abs(e.positions() - xo)) < 1e-12
+    _cells_exact(e, c)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_forces_thermalised_state(seed):
+    """Q13 on a disordered state: lattice jittered by up to 0.25 sigma, Gaussian
+    velocities, injected through dsea_set_state."""
+    e, c = _engine("C1")
+    g = _geom(c)
+    x = inputs.jitter(oracle.lattice(c.nx, c.ny, c.nz, g.a), g.b, 0.25, seed)
+    v = inputs.gaussian_velocities(c.n_atoms, 1.0, seed)
+    e.set_state(x, v)
+    _cells_exact(e, c)
+    e.step(1)
+    _, _, Fo, eo = oracle.run(x, v, np.zeros_like(x), g.b, c.rc, c.dt, 1)
+    _force_close(e.forces(), Fo)
+    _, en = e.energies()
+    assert np.allclose(en[-1, :3], eo[0, :3], rtol=1e-10)
+
+
+@pytest.mark.parametrize("cfg,seed", [("C1", 11289), ("C1", 5), ("P8", 7)])
+def test_positions_after_10_steps(cfg, seed):
+    """Q14: positions after 10 steps within 1e-8 sigma of the oracle; cells exact."""
+    e, c = _engine(cfg, seed=seed)
+    g = _geom(c)
+    x0, v0 = e.positions(), e.velocities()
+    e.step(10)
+    xo, vo, Fo, eo = oracle.run(x0, v0, np.zeros_like(x0), g.b, c.rc, c.dt, 10)
+    d = _min_image(e.positions() - xo, g.b)
+    assert np.max(np.abs(d)) < 1e-8
+    assert np.max(np.abs(e.velocities() - vo)) < 1e-8
+    _force_close(e.forces(), Fo, tol=1e-8)
+    _, en = e.energies()
+    assert np.allclose(en[:, 3], eo[:, 3], rtol=1e-10)
+    _cells_exact(e, c)
+
+
+def test_wall_hits_match_oracle():
+    """Mirror walls (reading Q2) against the oracle: edge atoms driven into
+    both walls, 60 steps, positions within 1e-8."""
+    e, c = _engine("C1")
+    g = _geom(c)
+    x = oracle.lattice(c.nx, c.ny, c.nz, g.a)
+    v = oracle.velocities(c.n_atoms, 9, 1.0)
+    v[x[:, 0] < 0.5 * g.a, 0] = -6.0
+    v[x[:, 0] > g.b[0] - 0.5 * g.a, 0] = 6.0
+    e.set_state(x, v)
+    e.step(60)
+    xo, vo, Fo, _ = oracle.run(x, v, np.zeros_like(x), g.b, c.rc, c.dt, 60)
+    assert np.max(np.abs(_min_image(e.positions() - xo, g.b))) < 1e-8
+    assert np.max(np.abs(e.velocities() - vo)) < 1e-7
+    _cells_exact(e, c)
+
+
+@pytest.mark.parametrize("rc,c_per,ns", [(4.0, 1, 0), (2.5, 2, 4), (2.5, 3, 0), (4.0, 2, 0)])
+def test_cutoff_and_slice_thickness_variants(rc, c_per, ns):
+    """C5-style variants at oracle size: rc = 4.0 and 2-3 cells per slice."""
+    from paper_2507_11289_b200.configs import Config
+    c = Config("v", 24 if rc < 3 else 30, 8, 8, ns, rc=rc, cells_per_slice_x=c_per)
+    g = _geom(c)
+    assert g.feasible
+    e, _ = _engine(c, seed=3)
+    x = inputs.jitter(oracle.lattice(c.nx, c.ny, c.nz, g.a), g.b, 0.15, 4)
+    v = inputs.gaussian_velocities(c.n_atoms, 0.8, 4)
+    e.set_state(x, v)
+    e.step(3)
+    xo, vo, Fo, eo = oracle.run(x, v, np.zeros_like(x), g.b, c.rc, c.dt, 3)
+    _force_close(e.forces(), Fo, tol=1e-9)
+    assert np.max(np.abs(_min_image(e.positions() - xo, g.b))) < 1e-10
+    _, en = e.energies()
+    assert np.allclose(en[:, 3], eo[:, 3], rtol=1e-10)
+    _cells_exact(e, c)
+
+
+@pytest.mark.parametrize("W,mode", [(1, D.DSEA_MODE_STAGED), (2, D.DSEA_MODE_STAGED), (3, D.DSEA_MODE_STAGED)])
+def test_ring_of_one_bitwise_equals_fused(W, mode):
+    """The stage schedule (Table 1, W workers sequential on one GPU) and the
+    fused whole-domain pass compute the same unit results: bitwise equal states
+    after 7 steps (7 is not a multiple of W = 2, 3: pass-through workers, Q15)."""
+    ref, c = _engine("P8")
+    ref.step(7)
+    e, _ = _engine("P8", workers_per_gpu=W, mode=mode)
+    e.step(7)
+    assert np.array_equal(e.positions(), ref.positions())
+    assert np.array_equal(e.velocities(), ref.velocities())
+    assert np.array_equal(e.forces(), ref.forces())
+    s1, e1 = ref.energies()
+    s2, e2 = e.energies()
+    assert s1.tolist() == s2.tolist() == list(range(7))
+    assert np.array_equal(e1, e2)
+
+
+def test_deterministic_rerun():
+    a, _ = _engine("C1")
+    b, _ = _engine("C1")
+    a.step(20)
+    b.step(10)
+    b.step(10)
+    assert np.array_equal(a.positions(), b.positions())
+    assert np.array_equal(a.energies()[1], b.energies()[1])
+
+
+@pytest.mark.slow
+def test_nve_energy_drift_1000_steps():
+    """North star: |dE/E| < 1e-4 over 1000 steps on C1 (Q19), and the GPU energy
+    series tracks the oracle's for the first 50 steps."""
+    e, c = _engine("C1")
+    g = _geom(c)
+    x0, v0 = e.positions(), e.velocities()
+    e.step(1000)
+    _, en = e.energies()
+    E = en[:, 3]
+    drift = np.max(np.abs(E - E[0])) / abs(E[0])
+    assert drift < 1e-4, drift
+    _, _, _, eo = oracle.run(x0, v0, np.zeros_like(x0), g.b, c.rc, c.dt, 50)
+    assert np.allclose(E[:50], eo[:, 3], rtol=1e-9)
+
+
+def test_full_size_c2_sampled_forces_and_cells():
+    """C2 (256,000 atoms, 64 slices) in the launch configuration bench.py times:
+    forces on 512 sampled atoms against the oracle's all-pairs sums, every atom's
+    cell bit-exact, atom count conserved."""
+    e, c = _engine("C2")
+    g = _geom(c)
+    x = inputs.jitter(oracle.lattice(c.nx, c.ny, c.nz, g.a), g.b, 0.2, 8)
+    v = inputs.gaussian_velocities(c.n_atoms, 1.0, 8)
+    e.set_state(x, v)
+    e.step(1)
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(c.n_atoms, 512, replace=False))
+    Fo, _ = oracle.forces_subset(x, g.b, c.rc, idx)
+    Fg = e.forces()[idx]
+    frms = np.sqrt((Fo ** 2).sum(1).mean())
+    err = np.sqrt(((Fg - Fo) ** 2).sum(1)) / np.maximum(np.sqrt((Fo ** 2).sum(1)), frms)
+    assert err.max() <= 1e-10
+    _cells_exact(e, c)
+
+
+def test_error_paths():
+    e, c = _engine("C1")
+    g = _geom(c)
+    # step 0 is a no-op
+    e.step(0)
+    assert e.energies()[0].size == 0
+    # outside the box -> EINVAL
+    x = oracle.lattice(c.nx, c.ny, c.nz, g.a)
+    v = np.zeros_like(x)
+    bad = x.copy()
+    bad[5, 1] = -1.0
+    with pytest.raises(D.DseaError) as ei:
+        e.set_state(bad, v)
+    assert ei.value.status == D.DSEA_EINVAL
+    # all atoms squeezed into slice 0 -> ECAPACITY
+    sq = x.copy()
+    sq[:, 0] = sq[:, 0] * (g.w * 0.99 / g.b[0])
+    with pytest.raises(D.DseaError) as ei:
+        e.set_state(sq, v)
+    assert ei.value.status == D.DSEA_ECAPACITY
+    # an atom jumping more than one slice -> EUNSTABLE
+    e2, _ = _engine("C1")
+    v2 = np.zeros_like(x)
+    v2[100, 0] = 5000.0
+    e2.set_state(x, v2)
+    with pytest.raises(D.DseaError) as ei:
+        e2.step(1)
+    assert ei.value.status == D.DSEA_EUNSTABLE
+    # stepping before slicing -> ESTATE
+    ctx = D.dsea_init(c.nx, c.ny, c.nz, c.rho, c.rc)
+    with pytest.raises(D.DseaError) as ei:
+        D.dsea_step(ctx, 1)
+    assert ei.value.status == D.DSEA_ESTATE
+    D.dsea_destroy(ctx)
