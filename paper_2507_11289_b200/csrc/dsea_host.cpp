@@ -312,8 +312,14 @@ void free_device(dsea_ctx* c)
     if (c->sliced) cudaSetDevice(c->device);
     if (c->connected) {
         if (nccl().ok) {
-            if (c->send_comm) nccl().CommDestroy(c->send_comm);
-            if (c->recv_comm) nccl().CommDestroy(c->recv_comm);
+            // ncclCommDestroy finalizes collectively: destroy the two link
+            // communicators in global link order (link r = rank r -> r+1) so that
+            // every pair of ranks meets in the same order (no cross-order deadlock).
+            const int send_link = c->rank, recv_link = (c->rank - 1 + c->NG) % c->NG;
+            ncclComm_t first = send_link < recv_link ? c->send_comm : c->recv_comm;
+            ncclComm_t second = send_link < recv_link ? c->recv_comm : c->send_comm;
+            if (first) nccl().CommDestroy(first);
+            if (second) nccl().CommDestroy(second);
         }
         c->send_comm = c->recv_comm = nullptr;
         c->connected = false;

@@ -18,6 +18,7 @@
 // depends only on the input slot contents.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include "dsea_internal.h"
 #include "../../include/dsea.h"
 
@@ -68,14 +69,19 @@ __device__ __forceinline__ int cell_coord(double r, double l, int n) {
 // ------------------------------------------------------------------------------
 // Force kernel.  One CTA = home cells [z0, z1) of column (cxl, cy) of slice j.
 // Stages the 9 neighbour columns over cells [z0-1, z1] (periodic images in y and z
-// pre-shifted, walls in x: absent columns) into shared memory, z-sorted, as FP32
-// (screen) and FP64 (exact) copies.  Warps take chunks of IL = 32/JPAR consecutive
-// home atoms; lane (il, par) screens every JPAR-th candidate of the chunk's z-window
-// in each column (one shared-memory broadcast per lane group), appends survivors to
-// its own hit list, and evaluates them in FP64.
+// pre-shifted; walls in x: absent columns) into shared memory, z-sorted, as FP64
+// (exact) and FP32 (screen) copies.  Every column run starts at an even index and
+// is padded to even length with a far-away dummy, so candidates are screened two
+// at a time with packed FP32x2 arithmetic.  Warps take chunks of IL = 32/JPAR
+// consecutive home atoms (dynamically, from a shared counter); lane (il, par)
+// screens every JPAR-th candidate pair of the chunk's z-window in each column
+// (shared-memory broadcast within a lane group), appends survivors to its own hit
+// list and evaluates them exactly in FP64.
 // ------------------------------------------------------------------------------
 constexpr int FORCE_THREADS = 128;
 constexpr int FORCE_WARPS = FORCE_THREADS / 32;
+
+__device__ __forceinline__ int stage_pad(int n) { return n + (n & 1); }
 
 template <int JPAR>
 __global__ void __launch_bounds__(FORCE_THREADS)
@@ -85,16 +91,20 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
 {
     constexpr int IL = 32 / JPAR;
     extern __shared__ __align__(16) unsigned char smem[];
-    float4* sp = reinterpret_cast<float4*>(smem);
-    double* sx = reinterpret_cast<double*>(sp + T.smax);
+    double* sx = reinterpret_cast<double*>(smem);
     double* sy = sx + T.smax;
     double* sz = sy + T.smax;
-    uint16_t* hl = reinterpret_cast<uint16_t*>(sz + T.smax);
+    float* fx32 = reinterpret_cast<float*>(sz + T.smax);
+    float* fy32 = fx32 + T.smax;
+    float* fz32 = fy32 + T.smax;
+    double4* chunk_e = reinterpret_cast<double4*>(fz32 + T.smax);   // [T.smax / IL + 1]
+    uint16_t* hl = reinterpret_cast<uint16_t*>(chunk_e + (T.smax / IL + 1));
 
-    __shared__ int p_slice[27], p_start[27], p_cnt[27], p_dst[27];
+    __shared__ int p_cnt[27], p_dst[27];
+    __shared__ const double* p_src[27][3];
     __shared__ double p_dy[27], p_dz[27];
     __shared__ int c_lo[9], c_hi[9];
-    __shared__ int s_total, s_home_first, s_nhome, s_self_base;
+    __shared__ int s_total, s_home_first, s_nhome, s_self_base, s_next_chunk;
     __shared__ double s_red[FORCE_WARPS][4];
     __shared__ bool s_last;
 
@@ -146,17 +156,24 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
                 }
             }
         }
-        // exclusive scan of counts over the 27 pieces (column-major => z-sorted runs)
-        int incl = cnt;
+        // column totals -> the last piece of each column carries the even padding
+        const int grp = lane - lane % 3;
+        int coltot = __shfl_sync(FULLMASK, cnt, grp) + __shfl_sync(FULLMASK, cnt, min(grp + 1, 31)) +
+                     __shfl_sync(FULLMASK, cnt, min(grp + 2, 31));
+        const int span = cnt + ((lane < 27 && lane % 3 == 2) ? (coltot & 1) : 0);
+        int incl = span;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             int v = __shfl_up_sync(FULLMASK, incl, o);
             if (lane >= o) incl += v;
         }
-        const int excl = incl - cnt;
+        const int excl = incl - span;
         if (lane < 27) {
-            p_slice[lane] = src_slice; p_start[lane] = start; p_cnt[lane] = cnt;
+            p_cnt[lane] = cnt;
             p_dst[lane] = excl; p_dy[lane] = dyv; p_dz[lane] = dzv;
+            p_src[lane][0] = slot_d(in, src_slice, in.L.off_x) + start;
+            p_src[lane][1] = slot_d(in, src_slice, in.L.off_y) + start;
+            p_src[lane][2] = slot_d(in, src_slice, in.L.off_z) + start;
         }
         if (lane == 31) s_total = incl;
         if (lane == 13) {
@@ -164,59 +181,73 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
             s_nhome = home_end - home_first;
             s_self_base = excl + (home_first - main_start);
         }
+        if (lane == 0) s_next_chunk = FORCE_WARPS;
     }
     __syncthreads();
     if (tid < 9) {
-        c_lo[tid] = p_dst[3 * tid];
-        c_hi[tid] = p_dst[3 * tid + 2] + p_cnt[3 * tid + 2];
+        const int lo = p_dst[3 * tid];
+        const int hi = p_dst[3 * tid + 2] + p_cnt[3 * tid + 2];
+        c_lo[tid] = lo;
+        c_hi[tid] = hi;
+        if ((hi - lo) & 1) {  // dummy far away: never passes the FP32 screen
+            fx32[hi] = 1e30f; fy32[hi] = 1e30f; fz32[hi] = 1e30f;
+            sx[hi] = 1e300; sy[hi] = 1e300; sz[hi] = 1e300;
+        }
     }
-    if (tid == 0 && tile == 0) {
-        stg.n[j] = slot_cs(in, j)[g.ncell];
-    }
+    if (tid == 0 && tile == 0) stg.n[j] = slot_cs(in, j)[g.ncell];
     const int total = s_total;
     if (total > T.smax) {
         if (tid == 0) set_err(err, DSEA_ECAPACITY, j, -1, total);
         return;
     }
 
-    // ---- stage neighbour atoms -----------------------------------------------------
-    for (int pc = 0; pc < 27; pc++) {
-        const int cnt = p_cnt[pc];
-        if (cnt == 0) continue;
-        const int m = p_slice[pc];
-        const double* gx = slot_d(in, m, in.L.off_x) + p_start[pc];
-        const double* gy = slot_d(in, m, in.L.off_y) + p_start[pc];
-        const double* gz = slot_d(in, m, in.L.off_z) + p_start[pc];
-        const double dyv = p_dy[pc], dzv = p_dz[pc];
-        const int dst = p_dst[pc];
-        for (int i = tid; i < cnt; i += FORCE_THREADS) {
-            const double x = gx[i];
-            const double y = gy[i] + dyv;
-            const double z = gz[i] + dzv;
-            sx[dst + i] = x; sy[dst + i] = y; sz[dst + i] = z;
-            sp[dst + i] = make_float4((float)(x - ox), (float)(y - oy), (float)(z - oz), 0.f);
+    // ---- stage neighbour atoms: warps take columns, lanes stride along a column -------
+    for (int col = warp; col < 9; col += FORCE_WARPS) {
+        const int n0 = p_cnt[3 * col], n1 = p_cnt[3 * col + 1], n2 = p_cnt[3 * col + 2];
+        const int dst = p_dst[3 * col];
+        const int n = n0 + n1 + n2;
+        const double* s0x = p_src[3 * col][0]; const double* s0y = p_src[3 * col][1]; const double* s0z = p_src[3 * col][2];
+        const double* s1x = p_src[3 * col + 1][0]; const double* s1y = p_src[3 * col + 1][1]; const double* s1z = p_src[3 * col + 1][2];
+        const double* s2x = p_src[3 * col + 2][0]; const double* s2y = p_src[3 * col + 2][1]; const double* s2z = p_src[3 * col + 2][2];
+        const double dy0 = p_dy[3 * col], dz0 = p_dz[3 * col], dz2 = p_dz[3 * col + 2];
+#pragma unroll 4
+        for (int t = lane; t < n; t += 32) {
+            const bool a0 = t < n0, a1 = !a0 && t < n0 + n1;
+            const int i = a0 ? t : a1 ? t - n0 : t - n0 - n1;
+            const double* px = a0 ? s0x : a1 ? s1x : s2x;
+            const double* py = a0 ? s0y : a1 ? s1y : s2y;
+            const double* pz = a0 ? s0z : a1 ? s1z : s2z;
+            const double x = __ldg(px + i);
+            const double y = __ldg(py + i) + dy0;
+            const double z = __ldg(pz + i) + (a0 ? dz0 : a1 ? 0.0 : dz2);
+            const int d = dst + t;
+            sx[d] = x; sy[d] = y; sz[d] = z;
+            fx32[d] = (float)(x - ox); fy32[d] = (float)(y - oy); fz32[d] = (float)(z - oz);
         }
     }
     __syncthreads();
 
     const int nhome = s_nhome, self_base = s_self_base, home_first = s_home_first;
     const int il = lane % IL, par = lane / IL;
-    const double rc = g.rc, rc2 = g.rc2;
     const float rc2s = g.rc2_screen;
+    const double rc2 = g.rc2;
     const int maxh = T.maxh;
-    constexpr int SEGC = 64;  // candidates per lane per segment upper bound check
-
-    double e_u = 0.0, e_v = 0.0, e_ke = 0.0;
-    int e_np = 0;
+    const float2* X2 = reinterpret_cast<const float2*>(fx32);
+    const float2* Y2 = reinterpret_cast<const float2*>(fy32);
+    const float2* Z2 = reinterpret_cast<const float2*>(fz32);
+    constexpr int SEG_PAIRS = 32;                       // candidate pairs per segment
+    constexpr int seg_need = 2 * ((SEG_PAIRS + JPAR - 1) / JPAR);  // max appends per lane
 
     const int nchunks = (nhome + IL - 1) / IL;
-    for (int ch = warp; ch < nchunks; ch += FORCE_WARPS) {
+    int ch = warp;
+    while (ch < nchunks) {
         const int q = ch * IL + il;
         const bool valid = q < nhome;
         const int si = self_base + (valid ? q : nhome - 1);
         const double xi = sx[si], yi = sy[si], zi = sz[si];
-        float4 pi = sp[si];
-        if (!valid) pi.x = 1e30f;
+        const float xf = valid ? fx32[si] : 1e30f, yf = fy32[si], zf = fz32[si];
+        const float2 xi2 = make_float2(xf, xf), yi2 = make_float2(yf, yf), zi2 = make_float2(zf, zf);
+        const float2 m1 = make_float2(-1.f, -1.f);
         const double zmin = sz[self_base + ch * IL];
         const double zmax = sz[self_base + min(ch * IL + IL, nhome) - 1];
 
@@ -225,18 +256,23 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
         if (lane < 9 || (lane >= 16 && lane < 25)) {
             const int col = lane < 9 ? lane : lane - 16;
             int lo = c_lo[col], hi = c_hi[col];
+            const int base = lo;
             if (lane < 9) {
-                const double key = zmin - rc - 1e-9;
+                const double key = zmin - g.rc - 1e-9;
                 while (lo < hi) { int mid = (lo + hi) >> 1; if (sz[mid] < key) lo = mid + 1; else hi = mid; }
+                wb = base + ((lo - base) & ~1);                // round down to the pair start
             } else {
-                const double key = zmax + rc + 1e-9;
+                const double key = zmax + g.rc + 1e-9;
                 while (lo < hi) { int mid = (lo + hi) >> 1; if (sz[mid] <= key) lo = mid + 1; else hi = mid; }
+                wb = base + ((lo - base + 1) & ~1);            // round up (may take the dummy)
             }
-            wb = lo;
         }
 
         double fx = 0.0, fy = 0.0, fz = 0.0;
+        double e_u = 0.0, e_v = 0.0, e_ke = 0.0;
+        int e_np = 0;
         int cnt = 0;
+        uint16_t* hp = hl + tid;
 
         auto flush = [&]() {
             for (int m = 0; m < cnt; m++) {
@@ -245,7 +281,7 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
                 const double dy = yi - sy[kk];
                 const double dz = zi - sz[kk];
                 const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-                if (r2 <= rc2) {  // inclusive cutoff
+                if (r2 <= rc2 && kk != si) {  // inclusive cutoff; i != j
                     const double s = rcp64(r2);
                     const double s3 = s * s * s;                // r^-6
                     const double t = fma(2.0, s3, -1.0);        // 2 r^-6 - 1
@@ -260,24 +296,33 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
                 }
             }
             cnt = 0;
+            hp = hl + tid;
         };
 
 #pragma unroll 1
         for (int col = 0; col < 9; col++) {
-            const int lo = __shfl_sync(FULLMASK, wb, col);
-            const int hi = __shfl_sync(FULLMASK, wb, 16 + col);
-            for (int s0 = lo; s0 < hi; s0 += SEGC * JPAR) {
-                const int e = min(hi, s0 + SEGC * JPAR);
-                const int need = (e - s0 + JPAR - 1) / JPAR;
-                if (__any_sync(FULLMASK, cnt + need > maxh)) flush();
-                for (int kk = s0 + par; kk < e; kk += JPAR) {
-                    const float4 p = sp[kk];
-                    const float dx = pi.x - p.x, dy = pi.y - p.y, dz = pi.z - p.z;
-                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                    if (r2 <= rc2s && kk != si) hl[(cnt++) * FORCE_THREADS + tid] = (uint16_t)kk;
+            const int plo = __shfl_sync(FULLMASK, wb, col) >> 1;
+            const int phi = __shfl_sync(FULLMASK, wb, 16 + col) >> 1;
+            for (int s0 = plo; s0 < phi; s0 += SEG_PAIRS) {
+                const int e = min(phi, s0 + SEG_PAIRS);
+                cnt = (int)(hp - (hl + tid)) / FORCE_THREADS;
+                if (__any_sync(FULLMASK, cnt + seg_need > maxh)) flush();
+#pragma unroll 4
+                for (int m = s0 + par; m < e; m += JPAR) {
+                    const float2 X = X2[m], Y = Y2[m], Z = Z2[m];
+                    const float2 dx = __ffma2_rn(X, m1, xi2);
+                    const float2 dy = __ffma2_rn(Y, m1, yi2);
+                    const float2 dz = __ffma2_rn(Z, m1, zi2);
+                    float2 r2 = __fmul2_rn(dz, dz);
+                    r2 = __ffma2_rn(dy, dy, r2);
+                    r2 = __ffma2_rn(dx, dx, r2);
+                    const int k = 2 * m;
+                    if (r2.x <= rc2s) { *hp = (uint16_t)k; hp += FORCE_THREADS; }
+                    if (r2.y <= rc2s) { *hp = (uint16_t)(k + 1); hp += FORCE_THREADS; }
                 }
             }
         }
+        cnt = (int)(hp - (hl + tid)) / FORCE_THREADS;
         flush();
 
         // combine the JPAR partial forces of each home atom (fixed xor tree)
@@ -333,28 +378,43 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
                 atomicAdd(&out_cnt[key], 1);
             }
         }
+        // chunk energies: fixed xor tree within the warp, stored by chunk index so the
+        // CTA total does not depend on which warp took which chunk
+        double np = (double)e_np;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            e_u += __shfl_xor_sync(FULLMASK, e_u, o);
+            e_v += __shfl_xor_sync(FULLMASK, e_v, o);
+            e_ke += __shfl_xor_sync(FULLMASK, e_ke, o);
+            np += __shfl_xor_sync(FULLMASK, np, o);
+        }
+        if (lane == 0) chunk_e[ch] = make_double4(e_u, e_v, e_ke, np);
+        // next chunk (dynamic: warps that finish early take more)
+        int nxt = 0;
+        if (lane == 0) nxt = atomicAdd(&s_next_chunk, 1);
+        ch = __shfl_sync(FULLMASK, nxt, 0);
     }
 
-    // ---- per-unit energies: fixed-order block reduction + last-CTA finish ------------
-    double np = (double)e_np;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        e_u += __shfl_xor_sync(FULLMASK, e_u, o);
-        e_v += __shfl_xor_sync(FULLMASK, e_v, o);
-        e_ke += __shfl_xor_sync(FULLMASK, e_ke, o);
-        np += __shfl_xor_sync(FULLMASK, np, o);
-    }
-    if (lane == 0) {
-        s_red[warp][0] = e_u; s_red[warp][1] = e_v; s_red[warp][2] = e_ke; s_red[warp][3] = np;
-    }
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {
         double a = 0, b = 0, c = 0, d = 0;
-        for (int w = 0; w < FORCE_WARPS; w++) { a += s_red[w][0]; b += s_red[w][1]; c += s_red[w][2]; d += s_red[w][3]; }
-        partials[(size_t)j * T.tiles + tile] = make_double4(a, b, c, d);
-        __threadfence();
-        const unsigned t = atomicAdd(&tickets[j], 1u);
-        s_last = (t == (unsigned)(T.tiles - 1));
+        for (int k = lane; k < nchunks; k += 32) {
+            const double4 p = chunk_e[k];
+            a += p.x; b += p.y; c += p.z; d += p.w;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(FULLMASK, a, o);
+            b += __shfl_xor_sync(FULLMASK, b, o);
+            c += __shfl_xor_sync(FULLMASK, c, o);
+            d += __shfl_xor_sync(FULLMASK, d, o);
+        }
+        if (lane == 0) {
+            partials[(size_t)j * T.tiles + tile] = make_double4(a, b, c, d);
+            __threadfence();
+            const unsigned t = atomicAdd(&tickets[j], 1u);
+            s_last = (t == (unsigned)(T.tiles - 1));
+        }
     }
     __syncthreads();
     if (s_last) {
@@ -546,39 +606,53 @@ __global__ void k_init_keys(Geo g, StgView stg, int n, int32_t* __restrict__ out
 // ------------------------------------------------------------------------------
 // Host-side launchers
 // ------------------------------------------------------------------------------
+static size_t force_smem_bytes(int smax, int jpar, int maxh)
+{
+    const int il = 32 / jpar;
+    return (size_t)smax * (3 * sizeof(double) + 3 * sizeof(float)) +
+           (size_t)(smax / il + 1) * sizeof(double4) + (size_t)maxh * FORCE_THREADS * sizeof(uint16_t);
+}
+
+static double env_num(const char* name, double dflt)
+{
+    const char* v = getenv(name);
+    return (v && *v) ? atof(v) : dflt;
+}
+
 Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
 {
+    // defaults from the B200 measurements in profiles/; DSEA_* overrides for sweeps
     Tiling T{};
-    T.jpar = 2;
-    T.maxh = 64;
+    T.jpar = (int)env_num("DSEA_JPAR", 2);
+    if (T.jpar != 2 && T.jpar != 4) T.jpar = 2;
+    T.maxh = (int)env_num("DSEA_MAXH", 64);
     const int CZ = g.cells[2];
-    const size_t per_atom = sizeof(float4) + 3 * sizeof(double);
-    const size_t lists = (size_t)T.maxh * FORCE_THREADS * sizeof(uint16_t);
-    const size_t budget = 72 * 1024;  // -> 3 CTAs per SM
-    int best_nzt = CZ;
-    for (int nzt = 1; nzt <= CZ; nzt++) {
-        const int tz = (CZ + nzt - 1) / nzt;
-        const double expected = 9.0 * (tz + 2) * mean_per_cell;
-        const int smax = ((int)(1.4 * expected + 96.0) + 31) / 32 * 32;
-        const size_t bytes = (size_t)smax * per_atom + lists;
-        if (bytes <= budget || nzt == CZ) { best_nzt = nzt; break; }
+    const size_t budget = (size_t)env_num("DSEA_SMEM_KB", 72) * 1024;
+    const double margin = env_num("DSEA_MARGIN", 1.35);
+    auto smax_for = [&](int tz) {
+        const double expected = 9.0 * (tz + 2) * mean_per_cell + 18.0;  // + even padding
+        return ((int)(margin * expected + 96.0) + 31) / 32 * 32;
+    };
+    int nzt = CZ;
+    for (int k = 1; k <= CZ; k++) {
+        const int tz = (CZ + k - 1) / k;
+        if (force_smem_bytes(smax_for(tz), T.jpar, T.maxh) <= budget) { nzt = k; break; }
     }
-    T.nzt = best_nzt;
-    T.tz = (CZ + T.nzt - 1) / T.nzt;
-    const double expected = 9.0 * (T.tz + 2) * mean_per_cell;
-    T.smax = ((int)(1.4 * expected + 96.0) + 31) / 32 * 32;
-    const size_t cap_atoms = (size_t)(smem_optin - (int)lists) / per_atom;
-    if ((size_t)T.smax > cap_atoms) T.smax = (int)cap_atoms;
-    if (T.smax > 65535) T.smax = 65535;  // uint16 hit-list indices
-    T.smem = (size_t)T.smax * per_atom + lists;
+    T.nzt = nzt;
+    T.tz = (CZ + nzt - 1) / nzt;
+    T.smax = smax_for(T.tz);
+    while (T.smax > 32 && force_smem_bytes(T.smax, T.jpar, T.maxh) > (size_t)smem_optin) T.smax -= 32;
+    if (T.smax > 65534) T.smax = 65504;  // uint16 hit-list indices
+    T.smem = force_smem_bytes(T.smax, T.jpar, T.maxh);
     T.tiles = g.c * g.cells[1] * T.nzt;
     return T;
 }
 
 int force_kernel_attr(const Tiling& T)
 {
-    cudaError_t e = cudaFuncSetAttribute(k_force<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)T.smem);
+    cudaError_t e = T.jpar == 4
+        ? cudaFuncSetAttribute(k_force<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem)
+        : cudaFuncSetAttribute(k_force<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem);
     return e == cudaSuccess ? 0 : -1;
 }
 
@@ -587,8 +661,12 @@ int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t
                  cudaStream_t s)
 {
     dim3 grid(T.tiles, nj);
-    k_force<2><<<grid, FORCE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, e_out, partials,
-                                                   tickets, err);
+    if (T.jpar == 4)
+        k_force<4><<<grid, FORCE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, e_out, partials,
+                                                       tickets, err);
+    else
+        k_force<2><<<grid, FORCE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, e_out, partials,
+                                                       tickets, err);
     return 1;
 }
 

@@ -1,0 +1,72 @@
+"""One rank of a multi-GPU ring check (launched by tests/test_gpu_ring.py through
+torchrun): slices stream through N_GPU processes, one GPU each, over NCCL links
+(§3.1).  Rank 0 writes the final state to an .npz for comparison with a
+single-GPU run of the same workload."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from paper_2507_11289_b200 import CONFIGS
+from paper_2507_11289_b200 import dsea as D
+
+
+def _log(rank, msg):
+    if os.environ.get("DSEA_RING_DEBUG"):
+        import time
+        print(f"[rank {rank} {time.time():.3f}] {msg}", flush=True)
+
+
+def main():
+    if os.environ.get("DSEA_RING_DEBUG"):
+        import faulthandler
+        import signal
+        faulthandler.register(signal.SIGTERM, all_threads=True)
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="P8")
+    ap.add_argument("--steps", type=int, default=16)
+    ap.add_argument("--workers", type=int, default=1)
+    ap.add_argument("--calls", type=int, default=1)
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args()
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = CONFIGS[a.config]
+    e = D.Engine(D.Box(c.nx, c.ny, c.nz, c.rho, c.rc, c.dt, c.T0, c.seed))
+    e.slice(n_slices=c.n_slices, cells_per_slice_x=c.cells_per_slice_x, n_gpus=world, rank=rank,
+            device=local, workers_per_gpu=a.workers)
+    _log(rank, "sliced")
+    ids = [b"".join(D.dsea_ring_unique_id() for _ in range(world))] if rank == 0 else [None]
+    dist.broadcast_object_list(ids, src=0)
+    _log(rank, "ids broadcast")
+    D.dsea_ring_connect(e.ctx, ids[0], world)
+    _log(rank, "connected")
+    per = a.steps // a.calls
+    for k in range(a.calls):
+        e.step(per if k < a.calls - 1 else a.steps - per * (a.calls - 1))
+        _log(rank, f"stepped call {k}")
+    steps, en = e.energies()
+    _log(rank, "energies")
+    allv = [None] * world
+    dist.all_gather_object(allv, (steps.tolist(), en.tolist()))
+    _log(rank, "gathered")
+    if rank == 0:
+        st = sorted((s, tuple(v)) for s_, v_ in allv for s, v in zip(s_, v_))
+        np.savez(a.out, x=e.positions(), v=e.velocities(), f=e.forces(),
+                 steps=np.array([s for s, _ in st]), en=np.array([v for _, v in st]),
+                 stats=np.array([e.stats().hop_bytes]))
+    dist.barrier()
+    e.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

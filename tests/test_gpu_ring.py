@@ -1,0 +1,66 @@
+"""Multi-GPU ring (one process per GPU, NCCL point-to-point links; §3.1,
+P:200-208 §3.4): the state after n steps equals the single-GPU run bit for bit --
+the ring is an exact re-scheduling of timesteps and every
+kernel result depends only on its input slots.  Needs >= 2 GPUs (gpurun --gpus N)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2507_11289_b200 import CONFIGS
+from paper_2507_11289_b200 import dsea as D
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _single(cfg, steps):
+    c = CONFIGS[cfg]
+    e = D.Engine(D.Box(c.nx, c.ny, c.nz, c.rho, c.rc, c.dt, c.T0, c.seed))
+    e.slice(n_slices=c.n_slices, cells_per_slice_x=c.cells_per_slice_x)
+    e.step(steps)
+    r = (e.positions(), e.velocities(), e.forces(), *e.energies())
+    e.close()
+    return r
+
+
+def _ring(tmp_path, n, cfg, steps, workers=1, calls=1):
+    out = str(tmp_path / f"ring_{n}_{cfg}_{steps}_{workers}_{calls}.npz")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + n * 7 + steps}",
+           os.path.join(ROOT, "tests", "ring_worker.py"), "--config", cfg, "--steps", str(steps),
+           "--workers", str(workers), "--calls", str(calls), "--out", out]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return np.load(out)
+
+
+CASES = [(2, "P8", 16, 1, 1), (2, "P8", 9, 1, 2), (2, "P8", 12, 2, 1), (4, "P8", 16, 1, 2),
+         (4, "P8", 10, 1, 1), (8, "P8", 16, 1, 1), (8, "C1", 8, 1, 1)]
+
+
+@pytest.mark.parametrize("n,cfg,steps,workers,calls", CASES)
+def test_ring_bitwise_equals_single_gpu(tmp_path, n, cfg, steps, workers, calls):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    c = CONFIGS[cfg]
+    if c.n_slices < 2 + 2 * workers:
+        pytest.skip("too few slices")
+    x, v, f, s1, e1 = _single(cfg, steps)
+    r = _ring(tmp_path, n, cfg, steps, workers, calls)
+    assert np.array_equal(r["x"], x)
+    assert np.array_equal(r["v"], v)
+    assert np.array_equal(r["f"], f)
+    assert r["steps"].tolist() == list(range(steps))
+    assert np.array_equal(r["en"], e1)
+    assert int(r["stats"][0]) > 0  # slices really crossed NVLink
