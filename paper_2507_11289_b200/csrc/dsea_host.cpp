@@ -364,6 +364,8 @@ dsea_status alloc_buf(dsea_ctx* c, BufView* B)
     if ((s = dalloc(c, &B->cnt, (size_t)c->g.ns * c->g.ncell))) return s;
     if ((s = dalloc(c, &B->perm, (size_t)c->g.ns * c->g.cap))) return s;
     CUDA_TRY(c, cudaMemset(B->cnt, 0, sizeof(int32_t) * (size_t)c->g.ns * c->g.ncell));
+    // zeroed scratch: after a reported error no later pass can index out of bounds
+    CUDA_TRY(c, cudaMemset(B->perm, 0, sizeof(int32_t) * (size_t)c->g.ns * c->g.cap));
     CUDA_TRY(c, cudaMemset(B->base, 0, c->L.slot_bytes * (size_t)c->g.ns));
     return DSEA_OK;
 }
@@ -378,6 +380,8 @@ dsea_status alloc_stg(dsea_ctx* c, StgView* S)
     if ((s = dalloc(c, &S->id, n))) return s;
     if ((s = dalloc(c, &S->key, n))) return s;
     if ((s = dalloc(c, &S->n, (size_t)c->g.ns))) return s;
+    CUDA_TRY(c, cudaMemset(S->key, 0, sizeof(int32_t) * n));
+    CUDA_TRY(c, cudaMemset(S->n, 0, sizeof(int32_t) * (size_t)c->g.ns));
     return DSEA_OK;
 }
 

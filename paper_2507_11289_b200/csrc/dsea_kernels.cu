@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
+#include <cmath>
+#include <algorithm>
 #include "dsea_internal.h"
 #include "../../include/dsea.h"
 
@@ -67,8 +69,9 @@ __device__ __forceinline__ int cell_coord(double r, double l, int n) {
 }
 
 // ------------------------------------------------------------------------------
-// Force kernel.  One CTA = home cells [z0, z1) of column (cxl, cy) of slice j.
-// Stages the 9 neighbour columns over cells [z0-1, z1] (periodic images in y and z
+// Force kernel.  One CTA = HOME_ATOMS consecutive (z-sorted) atoms of column (cxl, cy)
+// of slice j.  Stages the 9 neighbour columns over every cell within rc of them
+// (periodic images in y and z
 // pre-shifted; walls in x: absent columns) into shared memory, z-sorted, as FP64
 // (exact) and FP32 (screen) copies.  Every column run starts at an even index and
 // is padded to even length with a far-away dummy, so candidates are screened two
@@ -80,6 +83,7 @@ __device__ __forceinline__ int cell_coord(double r, double l, int n) {
 // ------------------------------------------------------------------------------
 constexpr int FORCE_THREADS = 128;
 constexpr int FORCE_WARPS = FORCE_THREADS / 32;
+constexpr int HOME_ATOMS = FORCE_WARPS * 16;   // home atoms per CTA: one 16-atom chunk per warp
 
 __device__ __forceinline__ int stage_pad(int n) { return n + (n & 1); }
 
@@ -97,8 +101,8 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
     float* fx32 = reinterpret_cast<float*>(sz + T.smax);
     float* fy32 = fx32 + T.smax;
     float* fz32 = fy32 + T.smax;
-    double4* chunk_e = reinterpret_cast<double4*>(fz32 + T.smax);   // [T.smax / IL + 1]
-    uint16_t* hl = reinterpret_cast<uint16_t*>(chunk_e + (T.smax / IL + 1));
+    double4* chunk_e = reinterpret_cast<double4*>(fz32 + T.smax);   // [T.smax / 16 + 65]
+    uint16_t* hl = reinterpret_cast<uint16_t*>(chunk_e + (T.smax / 16 + 65));
 
     __shared__ int p_cnt[27], p_dst[27];
     __shared__ const double* p_src[27][3];
@@ -112,290 +116,322 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
     const int j = j0 + blockIdx.y;
     const int tile = blockIdx.x;
     const int CY = g.cells[1], CZ = g.cells[2];
-    const int zt = tile % T.nzt;
+    const int tt = tile % T.nzt;                 // tile of HOME_ATOMS atoms within the column
     const int rest = tile / T.nzt;
     const int cyi = rest % CY;
     const int cxl = rest / CY;
-    const int z0 = (int)(((long long)zt * CZ) / T.nzt);
-    const int z1 = (int)(((long long)(zt + 1) * CZ) / T.nzt);
 
+    // home atoms: [h0, h1) of column (cxl, cyi) -- a fixed atom count per CTA so that
+    // every warp gets one chunk (the last tile of a column takes any remainder)
+    const int32_t* csj = slot_cs(in, j);
+    const int colbase_h = (cxl * CY + cyi) * CZ;
+    const int col_first = csj[colbase_h], col_end = csj[colbase_h + CZ];
+    const int h0 = col_first + tt * HOME_ATOMS;
+    const int h1 = (tt == T.nzt - 1) ? col_end : min(col_end, h0 + HOME_ATOMS);
+    const double* zj = slot_d(in, j, in.L.off_z);
     const double ox = (double)(j * g.c + cxl) * g.l[0];
     const double oy = (double)cyi * g.l[1];
-    const double oz = (double)z0 * g.l[2];
+    if (tid == 0 && tile == 0) stg.n[j] = slot_cs(in, j)[g.ncell];
 
+    int chunk_base = 0;
+    const int chunk_cap = T.smax / 16 + 64;
+    // sub-tiles: the home range is halved until its staged neighbourhood fits in
+    // shared memory (dense fluctuations never fail, they only cost an extra pass)
+    int hb = h0;
+    while (hb < h1) {
+        int he = h1;
+        double oz = 0.0;
+        for (;;) {
+            const double zfirst = zj[hb];
+            const double zlast = zj[he - 1];
+            oz = zfirst;
+            // staged z cells (inclusive): every cell within rc of a home atom; -1/CZ are images
+            const int z0 = (int)floor((zfirst - g.rc - 1e-9) / g.l[2]);
+            const int z1 = (int)floor((zlast + g.rc + 1e-9) / g.l[2]);
     // ---- piece table: 9 columns x {low wrap, main, high wrap} -------------------
-    if (warp == 0) {
-        int cnt = 0, src_slice = 0, start = 0;
-        double dyv = 0.0, dzv = 0.0;
-        int home_first = 0, home_end = 0, main_start = 0;
-        if (lane < 27) {
-            const int col = lane / 3, q = lane % 3;
-            const int dxk = col / 3 - 1, dyk = col % 3 - 1;
-            const int gx = j * g.c + cxl + dxk;
-            if (gx >= 0 && gx < g.cells[0]) {
-                const int m = gx / g.c, cx2 = gx - m * g.c;
-                int cyy = cyi + dyk;
-                if (cyy < 0) { cyy += CY; dyv = -g.b[1]; }
-                else if (cyy >= CY) { cyy -= CY; dyv = g.b[1]; }
-                const int zlo = z0 - 1, zhi = z1;  // inclusive
-                int a = 0, b = -1;
-                if (q == 0) { if (zlo < 0) { a = zlo + CZ; b = CZ - 1; dzv = -g.b[2]; } }
-                else if (q == 1) { a = max(zlo, 0); b = min(zhi, CZ - 1); }
-                else { if (zhi >= CZ) { a = 0; b = zhi - CZ; dzv = g.b[2]; } }
-                if (b >= a) {
-                    const int32_t* cs = slot_cs(in, m);
-                    const int colbase = (cx2 * CY + cyy) * CZ;
-                    start = cs[colbase + a];
-                    cnt = cs[colbase + b + 1] - start;
-                    src_slice = m;
-                    if (col == 4 && q == 1) {
-                        home_first = cs[colbase + z0];
-                        home_end = cs[colbase + z1];
-                        main_start = start;
+        if (warp == 0) {
+            int cnt = 0, src_slice = 0, start = 0;
+            double dyv = 0.0, dzv = 0.0;
+            int home_first = 0, home_end = 0, main_start = 0;
+            if (lane < 27) {
+                const int col = lane / 3, q = lane % 3;
+                const int dxk = col / 3 - 1, dyk = col % 3 - 1;
+                const int gx = j * g.c + cxl + dxk;
+                if (gx >= 0 && gx < g.cells[0]) {
+                    const int m = gx / g.c, cx2 = gx - m * g.c;
+                    int cyy = cyi + dyk;
+                    if (cyy < 0) { cyy += CY; dyv = -g.b[1]; }
+                    else if (cyy >= CY) { cyy -= CY; dyv = g.b[1]; }
+                    const int zlo = max(z0, -1), zhi = min(z1, CZ);  // inclusive
+                    int a = 0, b = -1;
+                    if (q == 0) { if (zlo < 0) { a = zlo + CZ; b = CZ - 1; dzv = -g.b[2]; } }
+                    else if (q == 1) { a = max(zlo, 0); b = min(zhi, CZ - 1); }
+                    else { if (zhi >= CZ) { a = 0; b = zhi - CZ; dzv = g.b[2]; } }
+                    if (b >= a) {
+                        const int32_t* cs = slot_cs(in, m);
+                        const int colbase = (cx2 * CY + cyy) * CZ;
+                        start = cs[colbase + a];
+                        cnt = cs[colbase + b + 1] - start;
+                        src_slice = m;
+                        if (col == 4 && q == 1) {
+                            home_first = hb;
+                            home_end = he;
+                            main_start = start;
+                        }
                     }
                 }
             }
+            // column totals -> the last piece of each column carries the even padding
+            const int grp = lane - lane % 3;
+            int coltot = __shfl_sync(FULLMASK, cnt, grp) + __shfl_sync(FULLMASK, cnt, min(grp + 1, 31)) +
+                         __shfl_sync(FULLMASK, cnt, min(grp + 2, 31));
+            const int span = cnt + ((lane < 27 && lane % 3 == 2) ? (coltot & 1) : 0);
+            int incl = span;
+    #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(FULLMASK, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int excl = incl - span;
+            if (lane < 27) {
+                p_cnt[lane] = cnt;
+                p_dst[lane] = excl; p_dy[lane] = dyv; p_dz[lane] = dzv;
+                p_src[lane][0] = slot_d(in, src_slice, in.L.off_x) + start;
+                p_src[lane][1] = slot_d(in, src_slice, in.L.off_y) + start;
+                p_src[lane][2] = slot_d(in, src_slice, in.L.off_z) + start;
+            }
+            if (lane == 31) s_total = incl;
+            if (lane == 13) {
+                s_home_first = home_first;
+                s_nhome = home_end - home_first;
+                s_self_base = excl + (home_first - main_start);
+            }
+            if (lane == 0) s_next_chunk = FORCE_WARPS;
         }
-        // column totals -> the last piece of each column carries the even padding
-        const int grp = lane - lane % 3;
-        int coltot = __shfl_sync(FULLMASK, cnt, grp) + __shfl_sync(FULLMASK, cnt, min(grp + 1, 31)) +
-                     __shfl_sync(FULLMASK, cnt, min(grp + 2, 31));
-        const int span = cnt + ((lane < 27 && lane % 3 == 2) ? (coltot & 1) : 0);
-        int incl = span;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int v = __shfl_up_sync(FULLMASK, incl, o);
-            if (lane >= o) incl += v;
+            __syncthreads();
+            if (s_total <= T.smax) break;
+            if (he - hb <= 16) {
+                if (tid == 0) set_err(err, DSEA_ECAPACITY, j, -1, s_total);
+                return;
+            }
+            he = hb + (((he - hb) / 2 + 15) & ~15);
+            __syncthreads();
         }
-        const int excl = incl - span;
-        if (lane < 27) {
-            p_cnt[lane] = cnt;
-            p_dst[lane] = excl; p_dy[lane] = dyv; p_dz[lane] = dzv;
-            p_src[lane][0] = slot_d(in, src_slice, in.L.off_x) + start;
-            p_src[lane][1] = slot_d(in, src_slice, in.L.off_y) + start;
-            p_src[lane][2] = slot_d(in, src_slice, in.L.off_z) + start;
+        if (tid < 9) {
+            const int lo = p_dst[3 * tid];
+            const int hi = p_dst[3 * tid + 2] + p_cnt[3 * tid + 2];
+            c_lo[tid] = lo;
+            c_hi[tid] = hi;
+            if ((hi - lo) & 1) {  // dummy far away: never passes the FP32 screen
+                fx32[hi] = 1e30f; fy32[hi] = 1e30f; fz32[hi] = 1e30f;
+                sx[hi] = 1e300; sy[hi] = 1e300; sz[hi] = 1e300;
+            }
         }
-        if (lane == 31) s_total = incl;
-        if (lane == 13) {
-            s_home_first = home_first;
-            s_nhome = home_end - home_first;
-            s_self_base = excl + (home_first - main_start);
-        }
-        if (lane == 0) s_next_chunk = FORCE_WARPS;
-    }
-    __syncthreads();
-    if (tid < 9) {
-        const int lo = p_dst[3 * tid];
-        const int hi = p_dst[3 * tid + 2] + p_cnt[3 * tid + 2];
-        c_lo[tid] = lo;
-        c_hi[tid] = hi;
-        if ((hi - lo) & 1) {  // dummy far away: never passes the FP32 screen
-            fx32[hi] = 1e30f; fy32[hi] = 1e30f; fz32[hi] = 1e30f;
-            sx[hi] = 1e300; sy[hi] = 1e300; sz[hi] = 1e300;
-        }
-    }
-    if (tid == 0 && tile == 0) stg.n[j] = slot_cs(in, j)[g.ncell];
-    const int total = s_total;
-    if (total > T.smax) {
-        if (tid == 0) set_err(err, DSEA_ECAPACITY, j, -1, total);
-        return;
-    }
-
     // ---- stage neighbour atoms: warps take columns, lanes stride along a column -------
-    for (int col = warp; col < 9; col += FORCE_WARPS) {
-        const int n0 = p_cnt[3 * col], n1 = p_cnt[3 * col + 1], n2 = p_cnt[3 * col + 2];
-        const int dst = p_dst[3 * col];
-        const int n = n0 + n1 + n2;
-        const double* s0x = p_src[3 * col][0]; const double* s0y = p_src[3 * col][1]; const double* s0z = p_src[3 * col][2];
-        const double* s1x = p_src[3 * col + 1][0]; const double* s1y = p_src[3 * col + 1][1]; const double* s1z = p_src[3 * col + 1][2];
-        const double* s2x = p_src[3 * col + 2][0]; const double* s2y = p_src[3 * col + 2][1]; const double* s2z = p_src[3 * col + 2][2];
-        const double dy0 = p_dy[3 * col], dz0 = p_dz[3 * col], dz2 = p_dz[3 * col + 2];
-#pragma unroll 4
-        for (int t = lane; t < n; t += 32) {
-            const bool a0 = t < n0, a1 = !a0 && t < n0 + n1;
-            const int i = a0 ? t : a1 ? t - n0 : t - n0 - n1;
-            const double* px = a0 ? s0x : a1 ? s1x : s2x;
-            const double* py = a0 ? s0y : a1 ? s1y : s2y;
-            const double* pz = a0 ? s0z : a1 ? s1z : s2z;
-            const double x = __ldg(px + i);
-            const double y = __ldg(py + i) + dy0;
-            const double z = __ldg(pz + i) + (a0 ? dz0 : a1 ? 0.0 : dz2);
-            const int d = dst + t;
-            sx[d] = x; sy[d] = y; sz[d] = z;
-            fx32[d] = (float)(x - ox); fy32[d] = (float)(y - oy); fz32[d] = (float)(z - oz);
+        for (int col = warp; col < 9; col += FORCE_WARPS) {
+            const int n0 = p_cnt[3 * col], n1 = p_cnt[3 * col + 1], n2 = p_cnt[3 * col + 2];
+            const int dst = p_dst[3 * col];
+            const int n = n0 + n1 + n2;
+            const double* s0x = p_src[3 * col][0]; const double* s0y = p_src[3 * col][1]; const double* s0z = p_src[3 * col][2];
+            const double* s1x = p_src[3 * col + 1][0]; const double* s1y = p_src[3 * col + 1][1]; const double* s1z = p_src[3 * col + 1][2];
+            const double* s2x = p_src[3 * col + 2][0]; const double* s2y = p_src[3 * col + 2][1]; const double* s2z = p_src[3 * col + 2][2];
+            const double dy0 = p_dy[3 * col], dz0 = p_dz[3 * col], dz2 = p_dz[3 * col + 2];
+    #pragma unroll 4
+            for (int t = lane; t < n; t += 32) {
+                const bool a0 = t < n0, a1 = !a0 && t < n0 + n1;
+                const int i = a0 ? t : a1 ? t - n0 : t - n0 - n1;
+                const double* px = a0 ? s0x : a1 ? s1x : s2x;
+                const double* py = a0 ? s0y : a1 ? s1y : s2y;
+                const double* pz = a0 ? s0z : a1 ? s1z : s2z;
+                const double x = __ldg(px + i);
+                const double y = __ldg(py + i) + dy0;
+                const double z = __ldg(pz + i) + (a0 ? dz0 : a1 ? 0.0 : dz2);
+                const int d = dst + t;
+                sx[d] = x; sy[d] = y; sz[d] = z;
+                fx32[d] = (float)(x - ox); fy32[d] = (float)(y - oy); fz32[d] = (float)(z - oz);
+            }
         }
-    }
-    __syncthreads();
-
+        __syncthreads();
+        {
     const int nhome = s_nhome, self_base = s_self_base, home_first = s_home_first;
-    const int il = lane % IL, par = lane / IL;
-    const float rc2s = g.rc2_screen;
-    const double rc2 = g.rc2;
-    const int maxh = T.maxh;
-    const float2* X2 = reinterpret_cast<const float2*>(fx32);
-    const float2* Y2 = reinterpret_cast<const float2*>(fy32);
-    const float2* Z2 = reinterpret_cast<const float2*>(fz32);
-    constexpr int SEG_PAIRS = 32;                       // candidate pairs per segment
-    constexpr int seg_need = 2 * ((SEG_PAIRS + JPAR - 1) / JPAR);  // max appends per lane
-
-    const int nchunks = (nhome + IL - 1) / IL;
-    int ch = warp;
-    while (ch < nchunks) {
-        const int q = ch * IL + il;
-        const bool valid = q < nhome;
-        const int si = self_base + (valid ? q : nhome - 1);
-        const double xi = sx[si], yi = sy[si], zi = sz[si];
-        const float xf = valid ? fx32[si] : 1e30f, yf = fy32[si], zf = fz32[si];
-        const float2 xi2 = make_float2(xf, xf), yi2 = make_float2(yf, yf), zi2 = make_float2(zf, zf);
-        const float2 m1 = make_float2(-1.f, -1.f);
-        const double zmin = sz[self_base + ch * IL];
-        const double zmax = sz[self_base + min(ch * IL + IL, nhome) - 1];
-
-        // z-windows of the chunk in each column (binary searches in parallel)
-        int wb = 0;
-        if (lane < 9 || (lane >= 16 && lane < 25)) {
-            const int col = lane < 9 ? lane : lane - 16;
-            int lo = c_lo[col], hi = c_hi[col];
-            const int base = lo;
-            if (lane < 9) {
-                const double key = zmin - g.rc - 1e-9;
-                while (lo < hi) { int mid = (lo + hi) >> 1; if (sz[mid] < key) lo = mid + 1; else hi = mid; }
-                wb = base + ((lo - base) & ~1);                // round down to the pair start
-            } else {
-                const double key = zmax + g.rc + 1e-9;
-                while (lo < hi) { int mid = (lo + hi) >> 1; if (sz[mid] <= key) lo = mid + 1; else hi = mid; }
-                wb = base + ((lo - base + 1) & ~1);            // round up (may take the dummy)
+            const int il = lane % IL, par = lane / IL;
+            const float rc2s = g.rc2_screen;
+            const double rc2 = g.rc2;
+            const int maxh = T.maxh;
+            const float2* X2 = reinterpret_cast<const float2*>(fx32);
+            const float2* Y2 = reinterpret_cast<const float2*>(fy32);
+            const float2* Z2 = reinterpret_cast<const float2*>(fz32);
+            constexpr int SEG_PAIRS = 32;                       // candidate pairs per segment
+            constexpr int seg_need = 2 * ((SEG_PAIRS + JPAR - 1) / JPAR);  // max appends per lane
+        
+            const int nchunks = (nhome + IL - 1) / IL;
+            if (chunk_base + nchunks > chunk_cap) {
+                if (tid == 0) set_err(err, DSEA_ECAPACITY, j, -1, chunk_base + nchunks);
+                return;
             }
-        }
-
-        double fx = 0.0, fy = 0.0, fz = 0.0;
-        double e_u = 0.0, e_v = 0.0, e_ke = 0.0;
-        int e_np = 0;
-        int cnt = 0;
-        uint16_t* hp = hl + tid;
-
-        auto flush = [&]() {
-            for (int m = 0; m < cnt; m++) {
-                const int kk = hl[m * FORCE_THREADS + tid];
-                const double dx = xi - sx[kk];
-                const double dy = yi - sy[kk];
-                const double dz = zi - sz[kk];
-                const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-                if (r2 <= rc2 && kk != si) {  // inclusive cutoff; i != j
-                    const double s = rcp64(r2);
-                    const double s3 = s * s * s;                // r^-6
-                    const double t = fma(2.0, s3, -1.0);        // 2 r^-6 - 1
-                    const double gq = s3 * t;                   // 2 r^-12 - r^-6
-                    const double f = s * gq;                    // F_abs / 24
-                    fx = fma(dx, f, fx);
-                    fy = fma(dy, f, fy);
-                    fz = fma(dz, f, fz);
-                    e_u += fma(s3, s3, -s3);                    // r^-12 - r^-6
-                    e_v += gq;                                  // 2 r^-12 - r^-6
-                    e_np += 1;
+            int ch = warp;
+            while (ch < nchunks) {
+                const int q = ch * IL + il;
+                const bool valid = q < nhome;
+                const int si = self_base + (valid ? q : nhome - 1);
+                const double xi = sx[si], yi = sy[si], zi = sz[si];
+                const float xf = valid ? fx32[si] : 1e30f, yf = fy32[si], zf = fz32[si];
+                const float2 xi2 = make_float2(xf, xf), yi2 = make_float2(yf, yf), zi2 = make_float2(zf, zf);
+                const float2 m1 = make_float2(-1.f, -1.f);
+                const double zmin = sz[self_base + ch * IL];
+                const double zmax = sz[self_base + min(ch * IL + IL, nhome) - 1];
+        
+                // z-windows of the chunk in each column (binary searches in parallel)
+                int wb = 0;
+                if (lane < 9 || (lane >= 16 && lane < 25)) {
+                    const int col = lane < 9 ? lane : lane - 16;
+                    int lo = c_lo[col], hi = c_hi[col];
+                    const int base = lo;
+                    if (lane < 9) {
+                        const double key = zmin - g.rc - 1e-9;
+                        while (lo < hi) { int mid = (lo + hi) >> 1; if (sz[mid] < key) lo = mid + 1; else hi = mid; }
+                        wb = base + ((lo - base) & ~1);                // round down to the pair start
+                    } else {
+                        const double key = zmax + g.rc + 1e-9;
+                        while (lo < hi) { int mid = (lo + hi) >> 1; if (sz[mid] <= key) lo = mid + 1; else hi = mid; }
+                        wb = base + ((lo - base + 1) & ~1);            // round up (may take the dummy)
+                    }
                 }
-            }
-            cnt = 0;
-            hp = hl + tid;
-        };
-
-#pragma unroll 1
-        for (int col = 0; col < 9; col++) {
-            const int plo = __shfl_sync(FULLMASK, wb, col) >> 1;
-            const int phi = __shfl_sync(FULLMASK, wb, 16 + col) >> 1;
-            for (int s0 = plo; s0 < phi; s0 += SEG_PAIRS) {
-                const int e = min(phi, s0 + SEG_PAIRS);
+        
+                double fx = 0.0, fy = 0.0, fz = 0.0;
+                double e_u = 0.0, e_v = 0.0, e_ke = 0.0;
+                int e_np = 0;
+                int cnt = 0;
+                uint16_t* hp = hl + tid;
+        
+                auto flush = [&]() {
+                    for (int m = 0; m < cnt; m++) {
+                        const int kk = hl[m * FORCE_THREADS + tid];
+                        const double dx = xi - sx[kk];
+                        const double dy = yi - sy[kk];
+                        const double dz = zi - sz[kk];
+                        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+                        if (r2 <= rc2 && kk != si) {  // inclusive cutoff; i != j
+                            const double s = rcp64(r2);
+                            const double s3 = s * s * s;                // r^-6
+                            const double t = fma(2.0, s3, -1.0);        // 2 r^-6 - 1
+                            const double gq = s3 * t;                   // 2 r^-12 - r^-6
+                            const double f = s * gq;                    // F_abs / 24
+                            fx = fma(dx, f, fx);
+                            fy = fma(dy, f, fy);
+                            fz = fma(dz, f, fz);
+                            e_u += fma(s3, s3, -s3);                    // r^-12 - r^-6
+                            e_v += gq;                                  // 2 r^-12 - r^-6
+                            e_np += 1;
+                        }
+                    }
+                    cnt = 0;
+                    hp = hl + tid;
+                };
+        
+        #pragma unroll 1
+                for (int col = 0; col < 9; col++) {
+                    const int plo = __shfl_sync(FULLMASK, wb, col) >> 1;
+                    const int phi = __shfl_sync(FULLMASK, wb, 16 + col) >> 1;
+                    for (int s0 = plo; s0 < phi; s0 += SEG_PAIRS) {
+                        const int e = min(phi, s0 + SEG_PAIRS);
+                        cnt = (int)(hp - (hl + tid)) / FORCE_THREADS;
+                        if (__any_sync(FULLMASK, cnt + seg_need > maxh)) flush();
+        #pragma unroll 4
+                        for (int m = s0 + par; m < e; m += JPAR) {
+                            const float2 X = X2[m], Y = Y2[m], Z = Z2[m];
+                            const float2 dx = __ffma2_rn(X, m1, xi2);
+                            const float2 dy = __ffma2_rn(Y, m1, yi2);
+                            const float2 dz = __ffma2_rn(Z, m1, zi2);
+                            float2 r2 = __fmul2_rn(dz, dz);
+                            r2 = __ffma2_rn(dy, dy, r2);
+                            r2 = __ffma2_rn(dx, dx, r2);
+                            const int k = 2 * m;
+                            if (r2.x <= rc2s) { *hp = (uint16_t)k; hp += FORCE_THREADS; }
+                            if (r2.y <= rc2s) { *hp = (uint16_t)(k + 1); hp += FORCE_THREADS; }
+                        }
+                    }
+                }
                 cnt = (int)(hp - (hl + tid)) / FORCE_THREADS;
-                if (__any_sync(FULLMASK, cnt + seg_need > maxh)) flush();
-#pragma unroll 4
-                for (int m = s0 + par; m < e; m += JPAR) {
-                    const float2 X = X2[m], Y = Y2[m], Z = Z2[m];
-                    const float2 dx = __ffma2_rn(X, m1, xi2);
-                    const float2 dy = __ffma2_rn(Y, m1, yi2);
-                    const float2 dz = __ffma2_rn(Z, m1, zi2);
-                    float2 r2 = __fmul2_rn(dz, dz);
-                    r2 = __ffma2_rn(dy, dy, r2);
-                    r2 = __ffma2_rn(dx, dx, r2);
-                    const int k = 2 * m;
-                    if (r2.x <= rc2s) { *hp = (uint16_t)k; hp += FORCE_THREADS; }
-                    if (r2.y <= rc2s) { *hp = (uint16_t)(k + 1); hp += FORCE_THREADS; }
+                flush();
+        
+                // combine the JPAR partial forces of each home atom (fixed xor tree)
+        #pragma unroll
+                for (int o = IL; o < 32; o <<= 1) {
+                    fx += __shfl_xor_sync(FULLMASK, fx, o);
+                    fy += __shfl_xor_sync(FULLMASK, fy, o);
+                    fz += __shfl_xor_sync(FULLMASK, fz, o);
                 }
+        
+                if (valid && par == 0) {
+                    // Algorithm 1: velocity update and position update
+                    const int gi = home_first + q;
+                    const double Fx = 24.0 * fx, Fy = 24.0 * fy, Fz = 24.0 * fz;
+                    const double fxo = slot_d(in, j, in.L.off_fx)[gi];
+                    const double fyo = slot_d(in, j, in.L.off_fy)[gi];
+                    const double fzo = slot_d(in, j, in.L.off_fz)[gi];
+                    double vx = slot_d(in, j, in.L.off_vx)[gi];
+                    double vy = slot_d(in, j, in.L.off_vy)[gi];
+                    double vz = slot_d(in, j, in.L.off_vz)[gi];
+                    const int id = slot_i(in, j, in.L.off_id)[gi];
+                    const double hdt = 0.5 * g.dt;
+                    vx = vx + (Fx + fxo) * hdt;
+                    vy = vy + (Fy + fyo) * hdt;
+                    vz = vz + (Fz + fzo) * hdt;
+                    e_ke += vx * vx + vy * vy + vz * vz;
+                    const double hdt2 = 0.5 * (g.dt * g.dt);
+                    double x = xi + vx * g.dt + Fx * hdt2;
+                    double y = yi + vy * g.dt + Fy * hdt2;
+                    double z = zi + vz * g.dt + Fz * hdt2;
+                    double Fxn = Fx;
+                    // x: mirror at 0 and b_x (reading Q2: fold r, negate v_x and F_x)
+                    if (x < 0.0) { x = -x; vx = -vx; Fxn = -Fxn; }
+                    else if (x > g.b[0]) { x = 2.0 * g.b[0] - x; vx = -vx; Fxn = -Fxn; }
+                    // y, z: periodic (Q1)
+                    if (y < 0.0) y += g.b[1]; else if (y >= g.b[1]) y -= g.b[1];
+                    if (z < 0.0) z += g.b[2]; else if (z >= g.b[2]) z -= g.b[2];
+                    // destination slice and cell (migration, md_v3b P:316-318)
+                    const int cxg = cell_coord(x, g.l[0], g.cells[0]);
+                    const int cyg = cell_coord(y, g.l[1], CY);
+                    const int czg = cell_coord(z, g.l[2], CZ);
+                    const int m = cxg / g.c;
+                    if (!(isfinite(x) && isfinite(y) && isfinite(z)) || m < j - 1 || m > j + 1) {
+                        set_err(err, DSEA_EUNSTABLE, j, id, m);
+                    } else {
+                        const int key = m * g.ncell + ((cxg - m * g.c) * CY + cyg) * CZ + czg;
+                        const size_t st = (size_t)j * g.cap + gi;
+                        stg.x[st] = x; stg.y[st] = y; stg.z[st] = z;
+                        stg.vx[st] = vx; stg.vy[st] = vy; stg.vz[st] = vz;
+                        stg.fx[st] = Fxn; stg.fy[st] = Fy; stg.fz[st] = Fz;
+                        stg.id[st] = id;
+                        stg.key[st] = key;
+                        atomicAdd(&out_cnt[key], 1);
+                    }
+                }
+                // chunk energies: fixed xor tree within the warp, stored by chunk index so the
+                // CTA total does not depend on which warp took which chunk
+                double np = (double)e_np;
+        #pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    e_u += __shfl_xor_sync(FULLMASK, e_u, o);
+                    e_v += __shfl_xor_sync(FULLMASK, e_v, o);
+                    e_ke += __shfl_xor_sync(FULLMASK, e_ke, o);
+                    np += __shfl_xor_sync(FULLMASK, np, o);
+                }
+                if (lane == 0) chunk_e[chunk_base + ch] = make_double4(e_u, e_v, e_ke, np);
+                // next chunk (dynamic: warps that finish early take more)
+                int nxt = 0;
+                if (lane == 0) nxt = atomicAdd(&s_next_chunk, 1);
+                ch = __shfl_sync(FULLMASK, nxt, 0);
             }
+        
         }
-        cnt = (int)(hp - (hl + tid)) / FORCE_THREADS;
-        flush();
-
-        // combine the JPAR partial forces of each home atom (fixed xor tree)
-#pragma unroll
-        for (int o = IL; o < 32; o <<= 1) {
-            fx += __shfl_xor_sync(FULLMASK, fx, o);
-            fy += __shfl_xor_sync(FULLMASK, fy, o);
-            fz += __shfl_xor_sync(FULLMASK, fz, o);
-        }
-
-        if (valid && par == 0) {
-            // Algorithm 1: velocity update and position update
-            const int gi = home_first + q;
-            const double Fx = 24.0 * fx, Fy = 24.0 * fy, Fz = 24.0 * fz;
-            const double fxo = slot_d(in, j, in.L.off_fx)[gi];
-            const double fyo = slot_d(in, j, in.L.off_fy)[gi];
-            const double fzo = slot_d(in, j, in.L.off_fz)[gi];
-            double vx = slot_d(in, j, in.L.off_vx)[gi];
-            double vy = slot_d(in, j, in.L.off_vy)[gi];
-            double vz = slot_d(in, j, in.L.off_vz)[gi];
-            const int id = slot_i(in, j, in.L.off_id)[gi];
-            const double hdt = 0.5 * g.dt;
-            vx = vx + (Fx + fxo) * hdt;
-            vy = vy + (Fy + fyo) * hdt;
-            vz = vz + (Fz + fzo) * hdt;
-            e_ke += vx * vx + vy * vy + vz * vz;
-            const double hdt2 = 0.5 * (g.dt * g.dt);
-            double x = xi + vx * g.dt + Fx * hdt2;
-            double y = yi + vy * g.dt + Fy * hdt2;
-            double z = zi + vz * g.dt + Fz * hdt2;
-            double Fxn = Fx;
-            // x: mirror at 0 and b_x (reading Q2: fold r, negate v_x and F_x)
-            if (x < 0.0) { x = -x; vx = -vx; Fxn = -Fxn; }
-            else if (x > g.b[0]) { x = 2.0 * g.b[0] - x; vx = -vx; Fxn = -Fxn; }
-            // y, z: periodic (Q1)
-            if (y < 0.0) y += g.b[1]; else if (y >= g.b[1]) y -= g.b[1];
-            if (z < 0.0) z += g.b[2]; else if (z >= g.b[2]) z -= g.b[2];
-            // destination slice and cell (migration, md_v3b P:316-318)
-            const int cxg = cell_coord(x, g.l[0], g.cells[0]);
-            const int cyg = cell_coord(y, g.l[1], CY);
-            const int czg = cell_coord(z, g.l[2], CZ);
-            const int m = cxg / g.c;
-            if (!(isfinite(x) && isfinite(y) && isfinite(z)) || m < j - 1 || m > j + 1) {
-                set_err(err, DSEA_EUNSTABLE, j, id, m);
-            } else {
-                const int key = m * g.ncell + ((cxg - m * g.c) * CY + cyg) * CZ + czg;
-                const size_t st = (size_t)j * g.cap + gi;
-                stg.x[st] = x; stg.y[st] = y; stg.z[st] = z;
-                stg.vx[st] = vx; stg.vy[st] = vy; stg.vz[st] = vz;
-                stg.fx[st] = Fxn; stg.fy[st] = Fy; stg.fz[st] = Fz;
-                stg.id[st] = id;
-                stg.key[st] = key;
-                atomicAdd(&out_cnt[key], 1);
-            }
-        }
-        // chunk energies: fixed xor tree within the warp, stored by chunk index so the
-        // CTA total does not depend on which warp took which chunk
-        double np = (double)e_np;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            e_u += __shfl_xor_sync(FULLMASK, e_u, o);
-            e_v += __shfl_xor_sync(FULLMASK, e_v, o);
-            e_ke += __shfl_xor_sync(FULLMASK, e_ke, o);
-            np += __shfl_xor_sync(FULLMASK, np, o);
-        }
-        if (lane == 0) chunk_e[ch] = make_double4(e_u, e_v, e_ke, np);
-        // next chunk (dynamic: warps that finish early take more)
-        int nxt = 0;
-        if (lane == 0) nxt = atomicAdd(&s_next_chunk, 1);
-        ch = __shfl_sync(FULLMASK, nxt, 0);
+        __syncthreads();
+        chunk_base += (s_nhome + 15) / 16;
+        hb = he;
     }
+    const int nchunks = chunk_base;
 
-    __syncthreads();
     if (warp == 0) {
         double a = 0, b = 0, c = 0, d = 0;
         for (int k = lane; k < nchunks; k += 32) {
@@ -610,7 +646,7 @@ static size_t force_smem_bytes(int smax, int jpar, int maxh)
 {
     const int il = 32 / jpar;
     return (size_t)smax * (3 * sizeof(double) + 3 * sizeof(float)) +
-           (size_t)(smax / il + 1) * sizeof(double4) + (size_t)maxh * FORCE_THREADS * sizeof(uint16_t);
+           (size_t)(smax / 16 + 64 + 1) * sizeof(double4) + (size_t)maxh * FORCE_THREADS * sizeof(uint16_t);
 }
 
 static double env_num(const char* name, double dflt)
@@ -623,24 +659,20 @@ Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
 {
     // defaults from the B200 measurements in profiles/; DSEA_* overrides for sweeps
     Tiling T{};
-    T.jpar = (int)env_num("DSEA_JPAR", 2);
-    if (T.jpar != 2 && T.jpar != 4) T.jpar = 2;
+    T.jpar = 2;
     T.maxh = (int)env_num("DSEA_MAXH", 64);
+    const double margin = env_num("DSEA_MARGIN", 1.25);
     const int CZ = g.cells[2];
-    const size_t budget = (size_t)env_num("DSEA_SMEM_KB", 72) * 1024;
-    const double margin = env_num("DSEA_MARGIN", 1.35);
-    auto smax_for = [&](int tz) {
-        const double expected = 9.0 * (tz + 2) * mean_per_cell + 18.0;  // + even padding
-        return ((int)(margin * expected + 96.0) + 31) / 32 * 32;
-    };
-    int nzt = CZ;
-    for (int k = 1; k <= CZ; k++) {
-        const int tz = (CZ + k - 1) / k;
-        if (force_smem_bytes(smax_for(tz), T.jpar, T.maxh) <= budget) { nzt = k; break; }
-    }
-    T.nzt = nzt;
-    T.tz = (CZ + nzt - 1) / nzt;
-    T.smax = smax_for(T.tz);
+    const double mean_col = mean_per_cell * CZ;               // atoms per column
+    const double dens = mean_per_cell / g.l[2];                // atoms per sigma of column
+    // tiles per column: HOME_ATOMS atoms each, with headroom for density fluctuations
+    T.nzt = std::max(1, (int)std::ceil(1.25 * mean_col / HOME_ATOMS) + 1);
+    T.tz = 0;
+    // staged atoms: 9 columns x (home extent + 2 rc + partial cells at both ends)
+    const double per_col = std::min(mean_col + 2.0 * mean_per_cell,
+                                    HOME_ATOMS + (2.0 * g.rc + g.l[2]) * dens);
+    const double expected = 9.0 * per_col + 18.0;
+    T.smax = ((int)(margin * expected + 96.0) + 31) / 32 * 32;
     while (T.smax > 32 && force_smem_bytes(T.smax, T.jpar, T.maxh) > (size_t)smem_optin) T.smax -= 32;
     if (T.smax > 65534) T.smax = 65504;  // uint16 hit-list indices
     T.smem = force_smem_bytes(T.smax, T.jpar, T.maxh);

@@ -42,3 +42,16 @@ if len(rows) > 2:
     print("  hottest SASS blocks (instr share / stall-sample share):")
     for b in sorted(blocks, key=lambda b: -(b[3] / tot + b[4] / ws))[:int(sys.argv[2]) if len(sys.argv) > 2 else 12]:
         print(f"   {b[0]:5d}-{b[1]:5d} x{b[2]:<9d} n={b[1]-b[0]+1:4d} inst={b[3]/tot*100:5.1f}% stall={b[4]/ws*100:5.1f}%  {data[b[0]][iS].strip()[:60]}")
+
+# ---- per-region stall reasons (regions split at barriers / big count changes) ----
+if len(sys.argv) > 3 and len(rows) > 2:
+    reasons = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
+    idx = {c: h.index(c) for c in reasons}
+    regs = [(int(a), int(b), n) for a, b, n in (x.split(":") for x in sys.argv[3].split(","))]
+    tot = {c: sum(int(r[idx[c]]) for r in data if r[idx[c]].isdigit()) for c in reasons}
+    allt = sum(tot.values())
+    for a, b, n in regs:
+        sub = {c: sum(int(r[idx[c]]) for r in data[a:b] if r[idx[c]].isdigit()) for c in reasons}
+        s = sum(sub.values())
+        top = sorted(sub.items(), key=lambda x: -x[1])[:5]
+        print(f"  {n:14s} {s/allt*100:5.1f}% of samples: " + ", ".join(f"{k[6:]}={v/allt*100:.1f}%" for k, v in top))
