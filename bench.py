@@ -43,6 +43,19 @@ FP64_LANES_PER_SM = 64
 N_SMS = 148
 
 
+def measured_traffic_per_atom():
+    """DRAM bytes per atom of the force kernel from the committed ncu capture (or None)."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "force_traffic.json"))):
+        try:
+            with open(f) as fh:
+                best = float(json.load(fh)["bytes_per_atom"])
+        except Exception:
+            pass
+    return best
+
+
 def peaks():
     try:
         with open(MEASURED_PEAKS) as f:
@@ -266,6 +279,7 @@ def main():
     fp64_achieved = pairs_per_atom * atoms_per_launch * FP64_FLOPS_PER_PAIR / (force_ms_avg * 1e-3) / 1e12
     hbm_achieved = FORCE_BYTES_PER_ATOM * atoms_per_launch / (force_ms_avg * 1e-3) / 1e9
     force_share = st.force_ms / max(1e-9, st.force_ms + st.bin_ms)
+    traffic_pa = measured_traffic_per_atom()
 
     # ---- e2e through the public API with host buffers ------------------------------
     e2e = None
@@ -315,7 +329,10 @@ def main():
                        "l2": "inputs larger than L2 (state %.2f GB)" % (atoms * 76 / 1e9),
                        "parallelism": f"ring{world}"},
             "roofline": {"bound": "alu", "achieved": fp64_achieved, "peak": fp64_peak,
-                         "unit": "TFLOP/s", "frac": fp64_achieved / fp64_peak, "traffic": None,
+                         "unit": "TFLOP/s", "frac": fp64_achieved / fp64_peak,
+                         "traffic": (None if traffic_pa is None else traffic_pa * atoms_per_launch),
+                         "traffic_note": "dram read+write bytes per launch: ncu per-atom figure "
+                                         "(profiles/r*/force_traffic.json) x atoms per launch",
                          "kernel": "k_force (force + kick + drift + migration key)",
                          "peak_note": f"FP64: {N_SMS} SMs x {FP64_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz",
                          "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
