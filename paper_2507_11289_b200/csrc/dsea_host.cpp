@@ -380,6 +380,7 @@ dsea_status alloc_stg(dsea_ctx* c, StgView* S)
     if ((s = dalloc(c, &S->id, n))) return s;
     if ((s = dalloc(c, &S->key, n))) return s;
     if ((s = dalloc(c, &S->n, (size_t)c->g.ns))) return s;
+    if ((s = dalloc(c, &S->eatom, n))) return s;
     CUDA_TRY(c, cudaMemset(S->key, 0, sizeof(int32_t) * n));
     CUDA_TRY(c, cudaMemset(S->n, 0, sizeof(int32_t) * (size_t)c->g.ns));
     return DSEA_OK;
@@ -527,9 +528,9 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             }
             cudaEvent_t t0 = nullptr, t1 = nullptr;
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
-            force_launch(c->g, c->T, in_of(w), c->stg[w], c->outb[w].cnt, j, 1,
-                         c->e_dev + (size_t)op.t_rel * ns, c->partials, c->tickets, c->err_dev, c->cs);
-            c->stats.kernel_launches++;
+            c->stats.kernel_launches +=
+                force_launch(c->g, c->T, in_of(w), c->stg[w], c->outb[w].cnt, j, 1,
+                             c->e_dev + (size_t)op.t_rel * ns, c->partials, c->tickets, c->err_dev, c->cs);
             c->stats.force_launches++;
             if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_FORCE, {t0, t1}}); }
             if (w == 0 && c->NG > 1) {
@@ -593,8 +594,8 @@ dsea_status run_fused(dsea_ctx* c, int64_t n_steps)
     for (int64_t t = 0; t < n_steps; t++) {
         cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr;
         if (c->timing) { t0 = tev(c); t1 = tev(c); t2 = tev(c); cudaEventRecord(t0, c->cs); }
-        force_launch(c->g, c->T, c->inb, c->stg[0], c->inb.cnt, 0, ns, c->e_dev + (size_t)t * ns,
-                     c->partials, c->tickets, c->err_dev, c->cs);
+        const int nl = force_launch(c->g, c->T, c->inb, c->stg[0], c->inb.cnt, 0, ns,
+                                    c->e_dev + (size_t)t * ns, c->partials, c->tickets, c->err_dev, c->cs);
         if (c->timing) cudaEventRecord(t1, c->cs);
         bin_scan_launch(c->g, c->inb, 0, ns, c->err_dev, c->cs);
         bin_place_launch(c->g, c->inb, c->stg[0], 0, ns, 0, 0, ns, c->err_dev, c->cs);
@@ -604,7 +605,7 @@ dsea_status run_fused(dsea_ctx* c, int64_t n_steps)
             c->tpairs.push_back({TK_FORCE, {t0, t1}});
             c->tpairs.push_back({TK_BIN, {t1, t2}});
         }
-        c->stats.kernel_launches += 4;
+        c->stats.kernel_launches += 3 + nl;
         c->stats.force_launches += 1;
     }
     return DSEA_OK;

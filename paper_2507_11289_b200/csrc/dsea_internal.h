@@ -69,6 +69,7 @@ struct StgView {
     double *x, *y, *z, *vx, *vy, *vz, *fx, *fy, *fz;
     int32_t *id, *key;
     int32_t* n;      // [ns] atoms staged per slice
+    double4* eatom;  // [ns*cap] per-atom (u_core, vir2, ke2, pairs) of the last force pass
 };
 
 // Force-kernel tiling (one CTA = one (cx_local, cy) column x tz cells of z).
@@ -80,6 +81,7 @@ struct Tiling {
     int jpar;        // candidate parity groups (lanes = 32/jpar atoms x jpar)
     int maxh;        // per-lane hit-list capacity
     size_t smem;     // dynamic shared memory bytes
+    bool pipe;       // persistent pipelined kernel (default) or the one-tile-per-CTA kernel
 };
 
 // Energy record of one (slice, timestep) unit.
@@ -99,6 +101,7 @@ struct DevErr {
 };
 
 // ---- kernel launchers (dsea_kernels.cu) ----------------------------------
+size_t pipe_smem_bytes(int smax, int maxh);
 int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t* out_cnt,
                  int j0, int nj, UnitEnergy* e_out, double4* partials, unsigned* tickets,
                  DevErr* err, cudaStream_t s);

@@ -482,6 +482,484 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
 }
 
 // ------------------------------------------------------------------------------
+// Persistent pipelined force kernel (default).  Same arithmetic and the same
+// per-atom summation order as k_force above, organised for latency hiding:
+//   * one producer warp per CTA walks the CTA's tiles (round robin over all tiles of
+//     slices [j0, j0+nj)), builds each tile's 27-piece table, and stages the 9
+//     neighbour columns into one of two shared-memory buffers;
+//   * four consumer warps pull 16-atom chunks from the current buffer and move on
+//     to the next buffer as soon as the chunks run out -- no CTA-wide barrier;
+//   * buffers change hands through mbarriers (full: producer -> consumers, empty:
+//     consumers -> producer).
+// Energies are written per atom (u, v, ke, pairs) and reduced per slice in a fixed
+// order by k_energy, so the result does not depend on which warp took which chunk.
+// ------------------------------------------------------------------------------
+constexpr int PIPE_CWARPS = 4;                      // consumer warps
+constexpr int PIPE_CT = 32 * PIPE_CWARPS;           // consumer threads (hit-list columns)
+constexpr int PIPE_THREADS = PIPE_CT + 64;          // + two producer warps
+constexpr int PIPE_HOME = PIPE_CWARPS * 16;         // home atoms per tile
+constexpr int PIPE_PAD = 64;                        // slack after each staged array
+
+struct PipeMeta {
+    int j, nhome, self_base, home_first, nchunks, end, next_chunk, pad;
+    int c_lo[9], c_hi[9];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// producer-side wait: back off so the poll loop does not steal issue slots from consumers
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+    unsigned ok = 0;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(256);
+    }
+}
+
+struct PipeBuf {
+    double *sx, *sy, *sz;
+    float *fx, *fy, *fz;
+};
+
+__device__ __forceinline__ PipeBuf pipe_buf(unsigned char* smem, int smax, int b) {
+    const size_t per = (size_t)smax * 3 * sizeof(double) + (size_t)(smax + PIPE_PAD) * 3 * sizeof(float);
+    unsigned char* base = smem + (size_t)b * per;
+    PipeBuf B;
+    B.sx = reinterpret_cast<double*>(base);
+    B.sy = B.sx + smax;
+    B.sz = B.sy + smax;
+    B.fx = reinterpret_cast<float*>(B.sz + smax);
+    B.fy = B.fx + smax + PIPE_PAD;
+    B.fz = B.fy + smax + PIPE_PAD;
+    return B;
+}
+
+size_t pipe_smem_bytes(int smax, int maxh)
+{
+    const size_t per = (size_t)smax * 3 * sizeof(double) + (size_t)(smax + PIPE_PAD) * 3 * sizeof(float);
+    return 2 * per + (size_t)maxh * PIPE_CT * sizeof(uint16_t);
+}
+
+__global__ void __launch_bounds__(PIPE_THREADS, 2)
+k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt, int j0, int nj,
+             DevErr* __restrict__ err)
+{
+    constexpr int IL = 16;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ PipeMeta meta[2];
+    __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2];
+    __shared__ int pt_dst[27], pt_end[27];                 // producer-private piece table
+    __shared__ const double* pt_x[27];
+    __shared__ const double* pt_y[27];
+    __shared__ const double* pt_z[27];
+    __shared__ double pt_dy[27], pt_dz[27];
+    uint16_t* hl = reinterpret_cast<uint16_t*>(smem + 2 * ((size_t)T.smax * 3 * sizeof(double) +
+                                                             (size_t)(T.smax + PIPE_PAD) * 3 * sizeof(float)));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int CY = g.cells[1], CZ = g.cells[2];
+    if (tid == 0) {
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&full_bar[b], 64);                // every producer lane arrives
+            mbar_init(&empty_bar[b], PIPE_CWARPS);      // one arrival per consumer warp
+        }
+    }
+    __syncthreads();
+
+    if (warp >= PIPE_CWARPS) {
+        // ============================ producer (2 warps) ============================
+        // warp P0 builds each tile's piece table; both producer warps stage it.
+        const int pw = warp - PIPE_CWARPS, pl = pw * 32 + lane;
+        __shared__ int sh_he, sh_ok, sh_total, sh_main_start, sh_main_dst;
+        int it = 0;
+        const long long ntiles = (long long)nj * T.tiles;
+        for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int j = j0 + (int)(t / T.tiles);
+            const int tile = (int)(t % T.tiles);
+            const int tt = tile % T.nzt;
+            const int rest = tile / T.nzt;
+            const int cyi = rest % CY;
+            const int cxl = rest / CY;
+            const int32_t* csj = slot_cs(in, j);
+            if (tile == 0 && pl == 0) stg.n[j] = csj[g.ncell];
+            const int colbase_h = (cxl * CY + cyi) * CZ;
+            const int col_first = csj[colbase_h], col_end = csj[colbase_h + CZ];
+            const int h0 = col_first + tt * PIPE_HOME;
+            const int h1 = (tt == T.nzt - 1) ? col_end : min(col_end, h0 + PIPE_HOME);
+            const double* zj = slot_d(in, j, in.L.off_z);
+            const double ox = (double)(j * g.c + cxl) * g.l[0];
+            const double oy = (double)cyi * g.l[1];
+            int hb = h0;
+            while (hb < h1) {
+                asm volatile("bar.sync 1, 64;" ::: "memory");   // previous staging done: pt_* free
+                double oz = zj[hb];
+                if (pw == 0) {
+                    int he = h1;
+                    int cnt = 0, start = 0, src_slice = 0, excl = 0, total = 0;
+                    double dyv = 0.0, dzv = 0.0;
+                    bool ok = true;
+                    for (;;) {
+                        const double zfirst = zj[hb];
+                        const double zlast = zj[he - 1];
+                        const int z0 = (int)floor((zfirst - g.rc - 1e-9) / g.l[2]);
+                        const int z1 = (int)floor((zlast + g.rc + 1e-9) / g.l[2]);
+                        cnt = 0; start = 0; src_slice = 0; dyv = 0.0; dzv = 0.0;
+                        if (lane < 27) {
+                            const int col = lane / 3, q = lane % 3;
+                            const int dxk = col / 3 - 1, dyk = col % 3 - 1;
+                            const int gx = j * g.c + cxl + dxk;
+                            if (gx >= 0 && gx < g.cells[0]) {
+                                const int m = gx / g.c, cx2 = gx - m * g.c;
+                                int cyy = cyi + dyk;
+                                if (cyy < 0) { cyy += CY; dyv = -g.b[1]; }
+                                else if (cyy >= CY) { cyy -= CY; dyv = g.b[1]; }
+                                const int zlo = max(z0, -1), zhi = min(z1, CZ);
+                                int a0 = 0, b0 = -1;
+                                if (q == 0) { if (zlo < 0) { a0 = zlo + CZ; b0 = CZ - 1; dzv = -g.b[2]; } }
+                                else if (q == 1) { a0 = max(zlo, 0); b0 = min(zhi, CZ - 1); }
+                                else { if (zhi >= CZ) { a0 = 0; b0 = zhi - CZ; dzv = g.b[2]; } }
+                                if (b0 >= a0) {
+                                    const int32_t* cs = slot_cs(in, m);
+                                    const int colbase = (cx2 * CY + cyy) * CZ;
+                                    start = cs[colbase + a0];
+                                    cnt = cs[colbase + b0 + 1] - start;
+                                    src_slice = m;
+                                }
+                            }
+                        }
+                        const int grp = lane - lane % 3;
+                        const int coltot = __shfl_sync(FULLMASK, cnt, grp) + __shfl_sync(FULLMASK, cnt, min(grp + 1, 31)) +
+                                           __shfl_sync(FULLMASK, cnt, min(grp + 2, 31));
+                        const int span = cnt + ((lane < 27 && lane % 3 == 2) ? (coltot & 1) : 0);
+                        int incl = span;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int v = __shfl_up_sync(FULLMASK, incl, o);
+                            if (lane >= o) incl += v;
+                        }
+                        excl = incl - span;
+                        total = __shfl_sync(FULLMASK, incl, 31);
+                        if (total <= T.smax) break;
+                        if (he - hb <= 16) { ok = false; break; }
+                        he = hb + (((he - hb) / 2 + 15) & ~15);
+                    }
+                    if (lane < 27) {
+                        pt_dst[lane] = excl;
+                        pt_end[lane] = excl + cnt;
+                        pt_x[lane] = slot_d(in, src_slice, in.L.off_x) + start;
+                        pt_y[lane] = slot_d(in, src_slice, in.L.off_y) + start;
+                        pt_z[lane] = slot_d(in, src_slice, in.L.off_z) + start;
+                        pt_dy[lane] = dyv;
+                        pt_dz[lane] = dzv;
+                    }
+                    if (lane == 13) { sh_main_start = start; sh_main_dst = excl; }
+                    if (lane == 0) { sh_he = he; sh_ok = ok ? 1 : 0; sh_total = total; }
+                }
+                asm volatile("bar.sync 1, 64;" ::: "memory");
+                const int he = sh_he, total = sh_total;
+                if (!sh_ok) {
+                    if (pl == 0) set_err(err, DSEA_ECAPACITY, j, -1, total);
+                    break;
+                }
+                // ---- claim a buffer ----
+                const int b = it & 1;
+                if (it >= 2) mbar_wait_sleep(&empty_bar[b], ((it >> 1) - 1) & 1);
+                const PipeBuf B = pipe_buf(smem, T.smax, b);
+                PipeMeta& M = meta[b];
+                if (pw == 0) {
+                    if (lane < 9) {
+                        const int lo = pt_dst[3 * lane], hi = pt_end[3 * lane + 2];
+                        M.c_lo[lane] = lo;
+                        M.c_hi[lane] = hi;
+                        if ((hi - lo) & 1) {  // far-away dummy: never passes the screen
+                            B.fx[hi] = 1e30f; B.fy[hi] = 1e30f; B.fz[hi] = 1e30f;
+                            B.sx[hi] = 1e300; B.sy[hi] = 1e300; B.sz[hi] = 1e300;
+                        }
+                    }
+                    if (lane == 0) {
+                        M.j = j;
+                        M.nhome = he - hb;
+                        M.home_first = hb;
+                        M.self_base = sh_main_dst + (hb - sh_main_start);
+                        M.nchunks = (he - hb + IL - 1) / IL;
+                        M.next_chunk = 0;
+                        M.end = 0;
+                    }
+                }
+                // ---- stage: 64 lanes, each resolves 4 indices, then 12 loads in flight ----
+                int pc = 0;
+                for (int base = pl; base < total; base += 256) {
+                    int pcs[4], off[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int sidx = base + 64 * u;
+                        while (pc < 26 && sidx >= pt_end[pc]) pc++;   // monotone piece cursor
+                        const bool ok = sidx < total && sidx >= pt_dst[pc] && sidx < pt_end[pc];
+                        pcs[u] = ok ? pc : -1;
+                        off[u] = sidx - pt_dst[pc];
+                    }
+                    double xv[4], yv[4], zv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        if (pcs[u] >= 0) {
+                            xv[u] = __ldg(pt_x[pcs[u]] + off[u]);
+                            yv[u] = __ldg(pt_y[pcs[u]] + off[u]);
+                            zv[u] = __ldg(pt_z[pcs[u]] + off[u]);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        if (pcs[u] >= 0) {
+                            const int d = base + 64 * u;
+                            const double x = xv[u], y = yv[u] + pt_dy[pcs[u]], z = zv[u] + pt_dz[pcs[u]];
+                            B.sx[d] = x; B.sy[d] = y; B.sz[d] = z;
+                            B.fx[d] = (float)(x - ox); B.fy[d] = (float)(y - oy); B.fz[d] = (float)(z - oz);
+                        }
+                    }
+                }
+                __syncwarp();
+                mbar_arrive(&full_bar[b]);  // 64 arrivals: each lane releases its own stores
+                it++;
+                hb = he;
+            }
+        }
+        // end marker
+        const int b = it & 1;
+        if (it >= 2) mbar_wait(&empty_bar[b], ((it >> 1) - 1) & 1);
+        if (pl == 0) meta[b].end = 1;
+        __syncwarp();
+        mbar_arrive(&full_bar[b]);
+        return;
+    }
+
+    // ================================ consumers ================================
+    const int il = lane % IL, par = lane / IL;
+    const float rc2s = g.rc2_screen;
+    const double rc2 = g.rc2;
+    const int maxh = T.maxh;
+    constexpr int SEG_PAIRS = 32;
+    constexpr int seg_need = SEG_PAIRS;     // max appends per lane per segment (JPAR = 2)
+    const float2 m1 = make_float2(-1.f, -1.f);
+    int it = 0;
+    for (;;) {
+        const int b = it & 1;
+        mbar_wait(&full_bar[b], (it >> 1) & 1);
+        PipeMeta& M = meta[b];
+        if (M.end) break;
+        const PipeBuf B = pipe_buf(smem, T.smax, b);
+        const int j = M.j, nhome = M.nhome, self_base = M.self_base, home_first = M.home_first;
+        const int nchunks = M.nchunks;
+        const float2* X2 = reinterpret_cast<const float2*>(B.fx);
+        const float2* Y2 = reinterpret_cast<const float2*>(B.fy);
+        const float2* Z2 = reinterpret_cast<const float2*>(B.fz);
+        for (;;) {
+            int chv = 0;
+            if (lane == 0) chv = atomicAdd(&M.next_chunk, 1);
+            const int ch = __shfl_sync(FULLMASK, chv, 0);
+            if (ch >= nchunks) break;
+            const int q = ch * IL + il;
+            const bool valid = q < nhome;
+            const int si = self_base + (valid ? q : nhome - 1);
+            const double xi = B.sx[si], yi = B.sy[si], zi = B.sz[si];
+            const float xf = valid ? B.fx[si] : 1e30f, yf = B.fy[si], zf = B.fz[si];
+            const float2 xi2 = make_float2(xf, xf), yi2 = make_float2(yf, yf), zi2 = make_float2(zf, zf);
+            const double zmin = B.sz[self_base + ch * IL];
+            const double zmax = B.sz[self_base + min(ch * IL + IL, nhome) - 1];
+            int wb = 0;
+            if (lane < 9 || (lane >= 16 && lane < 25)) {
+                const int col = lane < 9 ? lane : lane - 16;
+                int lo = M.c_lo[col], hi = M.c_hi[col];
+                const int base = lo;
+                if (lane < 9) {
+                    const double key = zmin - g.rc - 1e-9;
+                    while (lo < hi) { const int mid = (lo + hi) >> 1; if (B.sz[mid] < key) lo = mid + 1; else hi = mid; }
+                    wb = base + ((lo - base) & ~1);
+                } else {
+                    const double key = zmax + g.rc + 1e-9;
+                    while (lo < hi) { const int mid = (lo + hi) >> 1; if (B.sz[mid] <= key) lo = mid + 1; else hi = mid; }
+                    wb = base + ((lo - base + 1) & ~1);
+                }
+            }
+            // integration inputs of this lane's atom, loaded now, used after the pair work
+            const int gi = home_first + (valid ? q : 0);
+            double fxo = 0, fyo = 0, fzo = 0, vx0 = 0, vy0 = 0, vz0 = 0;
+            int aid = 0;
+            if (valid && par == 0) {
+                fxo = __ldg(slot_d(in, j, in.L.off_fx) + gi);
+                fyo = __ldg(slot_d(in, j, in.L.off_fy) + gi);
+                fzo = __ldg(slot_d(in, j, in.L.off_fz) + gi);
+                vx0 = __ldg(slot_d(in, j, in.L.off_vx) + gi);
+                vy0 = __ldg(slot_d(in, j, in.L.off_vy) + gi);
+                vz0 = __ldg(slot_d(in, j, in.L.off_vz) + gi);
+                aid = __ldg(slot_i(in, j, in.L.off_id) + gi);
+            }
+            double fx = 0.0, fy = 0.0, fz = 0.0, e_u = 0.0, e_v = 0.0;
+            int e_np = 0;
+            int ho = tid;                        // next free hit-list slot of this lane
+            auto flush = [&]() {
+                for (int o = tid; o < ho; o += PIPE_CT) {
+                    const int kk = hl[o];
+                    const double dx = xi - B.sx[kk];
+                    const double dy = yi - B.sy[kk];
+                    const double dz = zi - B.sz[kk];
+                    const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+                    if (r2 <= rc2 && kk != si) {      // inclusive cutoff; i != j
+                        const double s = rcp64(r2);
+                        const double s3 = s * s * s;
+                        const double t = fma(2.0, s3, -1.0);
+                        const double gq = s3 * t;
+                        const double f = s * gq;
+                        fx = fma(dx, f, fx);
+                        fy = fma(dy, f, fy);
+                        fz = fma(dz, f, fz);
+                        e_u += fma(s3, s3, -s3);
+                        e_v += gq;
+                        e_np += 1;
+                    }
+                }
+                ho = tid;
+            };
+            auto screen = [&](const float2 X, const float2 Y, const float2 Z, const int k) {
+                const float2 dx = __ffma2_rn(X, m1, xi2);
+                const float2 dy = __ffma2_rn(Y, m1, yi2);
+                const float2 dz = __ffma2_rn(Z, m1, zi2);
+                float2 r2 = __fmul2_rn(dz, dz);
+                r2 = __ffma2_rn(dy, dy, r2);
+                r2 = __ffma2_rn(dx, dx, r2);
+                if (r2.x <= rc2s) { hl[ho] = (uint16_t)k; ho += PIPE_CT; }
+                if (r2.y <= rc2s) { hl[ho] = (uint16_t)(k + 1); ho += PIPE_CT; }
+            };
+#pragma unroll 1
+            for (int col = 0; col < 9; col++) {
+                const int plo = __shfl_sync(FULLMASK, wb, col) >> 1;
+                const int phi = __shfl_sync(FULLMASK, wb, 16 + col) >> 1;
+                for (int s0 = plo; s0 < phi; s0 += SEG_PAIRS) {
+                    const int e = min(phi, s0 + SEG_PAIRS);
+                    if (__any_sync(FULLMASK, ho + seg_need * PIPE_CT > maxh * PIPE_CT)) flush();
+                    int m = s0 + par;
+                    for (; m + 6 < e; m += 8) {      // 4 pairs: all loads first
+                        const float2 Xa = X2[m], Xb = X2[m + 2], Xc = X2[m + 4], Xd = X2[m + 6];
+                        const float2 Ya = Y2[m], Yb = Y2[m + 2], Yc = Y2[m + 4], Yd = Y2[m + 6];
+                        const float2 Za = Z2[m], Zb = Z2[m + 2], Zc = Z2[m + 4], Zd = Z2[m + 6];
+                        screen(Xa, Ya, Za, 2 * m);
+                        screen(Xb, Yb, Zb, 2 * m + 4);
+                        screen(Xc, Yc, Zc, 2 * m + 8);
+                        screen(Xd, Yd, Zd, 2 * m + 12);
+                    }
+                    for (; m < e; m += 2) screen(X2[m], Y2[m], Z2[m], 2 * m);
+                }
+            }
+            flush();
+            // combine the two parity lanes of each atom (fixed order)
+            fx += __shfl_xor_sync(FULLMASK, fx, IL);
+            fy += __shfl_xor_sync(FULLMASK, fy, IL);
+            fz += __shfl_xor_sync(FULLMASK, fz, IL);
+            e_u += __shfl_xor_sync(FULLMASK, e_u, IL);
+            e_v += __shfl_xor_sync(FULLMASK, e_v, IL);
+            e_np += __shfl_xor_sync(FULLMASK, e_np, IL);
+            if (valid && par == 0) {
+                const double Fx = 24.0 * fx, Fy = 24.0 * fy, Fz = 24.0 * fz;
+                double vx = vx0, vy = vy0, vz = vz0;
+                const int id = aid;
+                const double hdt = 0.5 * g.dt;
+                vx = vx + (Fx + fxo) * hdt;
+                vy = vy + (Fy + fyo) * hdt;
+                vz = vz + (Fz + fzo) * hdt;
+                const double ke2 = vx * vx + vy * vy + vz * vz;
+                const double hdt2 = 0.5 * (g.dt * g.dt);
+                double x = xi + vx * g.dt + Fx * hdt2;
+                double y = yi + vy * g.dt + Fy * hdt2;
+                double z = zi + vz * g.dt + Fz * hdt2;
+                double Fxn = Fx;
+                if (x < 0.0) { x = -x; vx = -vx; Fxn = -Fxn; }                       // Q2
+                else if (x > g.b[0]) { x = 2.0 * g.b[0] - x; vx = -vx; Fxn = -Fxn; }
+                if (y < 0.0) y += g.b[1]; else if (y >= g.b[1]) y -= g.b[1];         // Q1
+                if (z < 0.0) z += g.b[2]; else if (z >= g.b[2]) z -= g.b[2];
+                const int cxg = cell_coord(x, g.l[0], g.cells[0]);
+                const int cyg = cell_coord(y, g.l[1], CY);
+                const int czg = cell_coord(z, g.l[2], CZ);
+                const int m = cxg / g.c;
+                const size_t st = (size_t)j * g.cap + gi;
+                stg.eatom[st] = make_double4(e_u, e_v, ke2, (double)e_np);
+                if (!(isfinite(x) && isfinite(y) && isfinite(z)) || m < j - 1 || m > j + 1) {
+                    set_err(err, DSEA_EUNSTABLE, j, id, m);
+                    stg.key[st] = -1;
+                } else {
+                    const int key = m * g.ncell + ((cxg - m * g.c) * CY + cyg) * CZ + czg;
+                    stg.x[st] = x; stg.y[st] = y; stg.z[st] = z;
+                    stg.vx[st] = vx; stg.vy[st] = vy; stg.vz[st] = vz;
+                    stg.fx[st] = Fxn; stg.fy[st] = Fy; stg.fz[st] = Fz;
+                    stg.id[st] = id;
+                    stg.key[st] = key;
+                    atomicAdd(&out_cnt[key], 1);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[b]);
+        it++;
+    }
+}
+
+// Per-slice energies in a fixed order: thread-strided sums, warp trees, warps in order.
+constexpr int ENERGY_THREADS = 256;
+
+__global__ void __launch_bounds__(ENERGY_THREADS)
+k_energy(Geo g, StgView stg, int j0, UnitEnergy* __restrict__ e_out)
+{
+    const int j = j0 + blockIdx.x;
+    const int n = stg.n[j];
+    const double4* e = stg.eatom + (size_t)j * g.cap;
+    double a = 0, b = 0, c = 0, d = 0;
+    for (int p = threadIdx.x; p < n; p += ENERGY_THREADS) {
+        const double4 v = e[p];
+        a += v.x; b += v.y; c += v.z; d += v.w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(FULLMASK, a, o);
+        b += __shfl_xor_sync(FULLMASK, b, o);
+        c += __shfl_xor_sync(FULLMASK, c, o);
+        d += __shfl_xor_sync(FULLMASK, d, o);
+    }
+    __shared__ double s[ENERGY_THREADS / 32][4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) { s[warp][0] = a; s[warp][1] = b; s[warp][2] = c; s[warp][3] = d; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double A = 0, B = 0, C = 0, D = 0;
+        for (int w = 0; w < ENERGY_THREADS / 32; w++) { A += s[w][0]; B += s[w][1]; C += s[w][2]; D += s[w][3]; }
+        UnitEnergy ue;
+        ue.u_core = A; ue.vir2 = B; ue.ke2 = C; ue.npairs = D;
+        e_out[j] = ue;
+    }
+}
+
+// ------------------------------------------------------------------------------
 // Bin pass 1: exclusive scan of the arrival counts of slot m -> cell_start; the
 // counters become cursors.  One CTA per slot.
 // ------------------------------------------------------------------------------
@@ -649,6 +1127,8 @@ static size_t force_smem_bytes(int smax, int jpar, int maxh)
            (size_t)(smax / 16 + 64 + 1) * sizeof(double4) + (size_t)maxh * FORCE_THREADS * sizeof(uint16_t);
 }
 
+static int pipe_grid = 0;  // persistent grid: SMs x resident CTAs (set by force_kernel_attr)
+
 static double env_num(const char* name, double dflt)
 {
     const char* v = getenv(name);
@@ -677,11 +1157,30 @@ Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
     if (T.smax > 65534) T.smax = 65504;  // uint16 hit-list indices
     T.smem = force_smem_bytes(T.smax, T.jpar, T.maxh);
     T.tiles = g.c * g.cells[1] * T.nzt;
+    T.pipe = env_num("DSEA_FORCE_V2", 0) == 0;
+    if (T.pipe) {
+        T.smax = ((int)(env_num("DSEA_PIPE_MARGIN", 1.2) * expected + 64.0) + 31) / 32 * 32;
+        while (T.smax > 32 && pipe_smem_bytes(T.smax, T.maxh) > (size_t)smem_optin) T.smax -= 32;
+        if (T.smax > 65504) T.smax = 65504;
+        T.smem = pipe_smem_bytes(T.smax, T.maxh);
+    }
     return T;
 }
 
 int force_kernel_attr(const Tiling& T)
 {
+    if (T.pipe) {
+        cudaError_t e = cudaFuncSetAttribute(k_force_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)T.smem);
+        if (e != cudaSuccess) return -1;
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force_pipe, PIPE_THREADS, T.smem);
+        if (per_sm < 1) return -1;
+        pipe_grid = sms * per_sm;
+        return 0;
+    }
     cudaError_t e = T.jpar == 4
         ? cudaFuncSetAttribute(k_force<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem)
         : cudaFuncSetAttribute(k_force<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem);
@@ -692,6 +1191,11 @@ int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t
                  int nj, UnitEnergy* e_out, double4* partials, unsigned* tickets, DevErr* err,
                  cudaStream_t s)
 {
+    if (T.pipe) {
+        k_force_pipe<<<pipe_grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err);
+        k_energy<<<nj, ENERGY_THREADS, 0, s>>>(g, stg, j0, e_out);
+        return 2;
+    }
     dim3 grid(T.tiles, nj);
     if (T.jpar == 4)
         k_force<4><<<grid, FORCE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, e_out, partials,
