@@ -76,6 +76,9 @@ typedef struct {
     int32_t device;            /* CUDA device ordinal for this context */
     int32_t workers_per_gpu;   /* W = N_wGPU >= 1 */
     int32_t mode;              /* DSEA_MODE_* below */
+    int32_t slices_per_stage;  /* B >= 1 consecutive slices handled per stage (B = 1 is the
+                                  paper's Table 1 schedule); 0 -> auto: enough atoms per
+                                  launch, while keeping >= N_GPU*(2+W) blocks per super-cycle */
     double capacity_factor;    /* slot capacity / mean atoms per slice; 0 -> 1.25 */
 } dsea_slice_params;
 

@@ -69,12 +69,17 @@ NcclApi& nccl()
 }
 
 // ------------------------------------------------------------------------------
-// Stage schedule (Table 1 generalised).  Items are (cycle, slice) pairs in flat
-// order p = K*N_S + j.  At stage k of a rank: receive item k; worker w processes
-// item k-2-2w and finalises (bins) item k-3-2w; the last worker hands item
-// k-1-2W to the ring successor.  Worker w of rank g in cycle K computes timestep
-// K*N_w + g*W + w, or passes the slice through unchanged when that timestep is
-// beyond the requested count (Q15).
+// Stage schedule (Table 1 generalised).  The slices of a super-cycle are grouped in
+// blocks of B consecutive slices (B = 1 is the paper's schedule); flat blocks
+// p = K*nblk + c run over the super-cycles K.  At stage k of a rank: receive block
+// k; worker w processes block k-2-d*w (d = 2 for B = 1, d = 1 for B >= 2: a block's
+// right neighbour slice is final one block earlier) and then finalises (bins) the
+// slices whose three contributing units are done -- the last slice of the
+// previous block and all but the last slice of this block; the last worker hands
+// finalised slices to the ring successor.  Worker w of rank g in super-cycle K
+// computes timestep K*N_w + g*W + w, or passes the block through unchanged when
+// that timestep is beyond the requested count (Q15).  For B = 1 this is exactly
+// Table 1: receive k, process k-2, send k-3.
 // ------------------------------------------------------------------------------
 enum OpKind { OP_RECV = 0, OP_FORCE, OP_PASS, OP_BIN, OP_SEND };
 
@@ -82,7 +87,8 @@ struct Op {
     int kind;
     int stage;
     int worker;
-    int slice;
+    int slice;      // first slice
+    int count;      // number of consecutive slices
     int cycle;
     int64_t t_rel;  // timestep relative to the start of the call (FORCE only)
 };
@@ -92,42 +98,59 @@ struct Plan {
     int n_stages = 0;
 };
 
-Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps)
+Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps, int B)
 {
     Plan P;
+    if (B < 1) B = 1;
+    const int nblk = (ns + B - 1) / B;
+    const int d = (B == 1) ? 2 : 1;
     const int64_t nw = (int64_t)ng * W;
     const int64_t n_cycles = n_steps <= 0 ? 0 : (n_steps + nw - 1) / nw;
-    const int64_t items = n_cycles * ns;
+    const int64_t items = n_cycles * nblk;
     if (items == 0) return P;
     auto active = [&](int64_t K, int w) { return K * nw + (int64_t)rank * W + w < n_steps; };
-    // receive set
-    int64_t r_lo = 0, r_hi = 0;  // items received at stage == item index
+    auto blk_first = [&](int c) { return c * B; };
+    auto blk_count = [&](int c) { return std::min(B, ns - c * B); };
+    int64_t r_lo = 0, r_hi = 0;  // flat blocks received at stage == block index
     if (ng > 1) {
-        if (rank == 0) { r_lo = ns; r_hi = items + ns; }
+        if (rank == 0) { r_lo = nblk; r_hi = items + nblk; }
         else { r_lo = 0; r_hi = items; }
     }
-    const int64_t last_compute = items - 1 + 3 + 2 * (int64_t)(W - 1);
+    const int64_t last_compute = items + 2 + (int64_t)d * (W - 1);  // finalises the last slice
     const int64_t last_stage = std::max<int64_t>(last_compute, r_hi - 1);
     for (int64_t k = 0; k <= last_stage; k++) {
         if (k >= r_lo && k < r_hi) {
-            P.ops.push_back({OP_RECV, (int)k, -1, (int)(k % ns), (int)(k / ns), -1});
+            const int c = (int)(k % nblk);
+            for (int s = 0; s < blk_count(c); s++)
+                P.ops.push_back({OP_RECV, (int)k, -1, blk_first(c) + s, 1, (int)(k / nblk), -1});
         }
         for (int w = 0; w < W; w++) {
-            const int64_t p = k - 2 - 2 * (int64_t)w;
-            if (p >= 0 && p < items) {
-                const int64_t K = p / ns;
-                const int j = (int)(p % ns);
+            const int64_t p = k - 2 - (int64_t)d * w;
+            if (p < 0 || p > items) continue;
+            if (p < items) {
+                const int64_t K = p / nblk;
+                const int c = (int)(p % nblk);
                 if (active(K, w))
-                    P.ops.push_back({OP_FORCE, (int)k, w, j, (int)K, K * nw + (int64_t)rank * W + w});
+                    P.ops.push_back({OP_FORCE, (int)k, w, blk_first(c), blk_count(c), (int)K,
+                                     K * nw + (int64_t)rank * W + w});
                 else
-                    P.ops.push_back({OP_PASS, (int)k, w, j, (int)K, -1});
+                    P.ops.push_back({OP_PASS, (int)k, w, blk_first(c), blk_count(c), (int)K, -1});
             }
-            const int64_t q = k - 3 - 2 * (int64_t)w;
-            if (q >= 0 && q < items) {
-                const int64_t K = q / ns;
-                const int m = (int)(q % ns);
-                if (active(K, w)) P.ops.push_back({OP_BIN, (int)k, w, m, (int)K, -1});
-                if (w == W - 1) P.ops.push_back({OP_SEND, (int)k, w, m, (int)K, -1});
+            // finalise: last slice of block p-1, then the first count-1 slices of block p
+            auto fin = [&](int64_t K, int first, int cnt) {
+                if (cnt <= 0) return;
+                if (active(K, w)) P.ops.push_back({OP_BIN, (int)k, w, first, cnt, (int)K, -1});
+                if (w == W - 1)
+                    for (int s = 0; s < cnt; s++) P.ops.push_back({OP_SEND, (int)k, w, first + s, 1, (int)K, -1});
+            };
+            const bool same_cycle = p >= 1 && p < items && (p % nblk) != 0;
+            if (same_cycle) {
+                const int64_t K = p / nblk;
+                const int c = (int)(p % nblk);
+                fin(K, blk_first(c) - 1, blk_count(c));  // [first-1, first+count-2]
+            } else {
+                if (p >= 1) fin((p - 1) / nblk, ns - 1, 1);
+                if (p < items) fin(p / nblk, 0, blk_count(0) - 1);
             }
         }
     }
@@ -152,9 +175,9 @@ struct dsea_ctx {
     Tiling T{};
     SlotLayout L{};
     int mode = DSEA_MODE_FUSED;
-    int W = 1, NG = 1, rank = 0, device = 0;
+    int W = 1, NG = 1, rank = 0, device = 0, B = 1;
 
-    cudaStream_t cs = nullptr, ss = nullptr, rs = nullptr;
+    cudaStream_t cs = nullptr, ss = nullptr, rs = nullptr, es = nullptr;  // compute, send, recv, energy
     BufView inb{};
     std::vector<BufView> outb;
     std::vector<StgView> stg;
@@ -164,7 +187,10 @@ struct dsea_ctx {
     double4* partials = nullptr;
     unsigned* tickets = nullptr;
     DevErr* err_dev = nullptr;
+    unsigned long long* tile_ctr = nullptr;
+    unsigned long long tile_ctr_base = 0;
     std::vector<cudaEvent_t> ev_recv, ev_free, ev_bin, ev_send;
+    std::vector<cudaEvent_t> ev_force, ev_energy;   // per worker: force done / energies done
 
     bool connected = false;
     ncclComm_t send_comm = nullptr, recv_comm = nullptr;
@@ -336,7 +362,11 @@ void free_device(dsea_ctx* c)
     if (c->cs) cudaStreamDestroy(c->cs);
     if (c->ss) cudaStreamDestroy(c->ss);
     if (c->rs) cudaStreamDestroy(c->rs);
-    c->cs = c->ss = c->rs = nullptr;
+    if (c->es) cudaStreamDestroy(c->es);
+    for (cudaEvent_t e : c->ev_force) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_energy) cudaEventDestroy(e);
+    c->ev_force.clear(); c->ev_energy.clear();
+    c->cs = c->ss = c->rs = c->es = nullptr;
     c->e_dev = nullptr; c->e_cap = 0;
     c->outb.clear(); c->stg.clear();
     c->sliced = false;
@@ -504,83 +534,124 @@ enum { TK_FORCE = 0, TK_BIN = 1, TK_SEND = 2 };
 dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
 {
     const int ns = c->g.ns;
-    const Plan P = build_plan(ns, c->NG, c->rank, c->W, n_steps);
+    const Plan P = build_plan(ns, c->NG, c->rank, c->W, n_steps, c->B);
     std::vector<char> sent(ns, 0);
     const size_t sb = c->L.slot_bytes;
     NcclApi& api = nccl();
     const int W = c->W;
     auto in_of = [&](int w) -> BufView& { return w == 0 ? c->inb : c->outb[w - 1]; };
-    for (const Op& op : P.ops) {
+    const size_t nops = P.ops.size();
+    for (size_t oi = 0; oi < nops; oi++) {
+        const Op& op = P.ops[oi];
         switch (op.kind) {
         case OP_RECV: {
-            char* dst = c->inb.base + (size_t)op.slice * sb;
-            CUDA_TRY(c, cudaStreamWaitEvent(c->rs, c->ev_free[op.slice], 0));
-            ncclResult_t r = api.Recv(dst, sb, ncclChar, 0, c->recv_comm, c->rs);
-            if (r != ncclSuccess) return fail(c, DSEA_EPEER, "ncclRecv: %s", api.GetErrorString(r));
-            CUDA_TRY(c, cudaEventRecord(c->ev_recv[op.slice], c->rs));
+            // all receives of this stage in one NCCL group (matched by order with the
+            // predecessor's sends, one message per slice)
+            size_t oe = oi;
+            while (oe < nops && P.ops[oe].kind == OP_RECV && P.ops[oe].stage == op.stage) oe++;
+            for (size_t q = oi; q < oe; q++)
+                CUDA_TRY(c, cudaStreamWaitEvent(c->rs, c->ev_free[P.ops[q].slice], 0));
+            api.GroupStart();
+            for (size_t q = oi; q < oe; q++) {
+                ncclResult_t r = api.Recv(c->inb.base + (size_t)P.ops[q].slice * sb, sb, ncclChar, 0,
+                                          c->recv_comm, c->rs);
+                if (r != ncclSuccess) { api.GroupEnd(); return fail(c, DSEA_EPEER, "ncclRecv: %s", api.GetErrorString(r)); }
+            }
+            ncclResult_t r = api.GroupEnd();
+            if (r != ncclSuccess) return fail(c, DSEA_EPEER, "ncclGroupEnd (recv): %s", api.GetErrorString(r));
+            for (size_t q = oi; q < oe; q++) CUDA_TRY(c, cudaEventRecord(c->ev_recv[P.ops[q].slice], c->rs));
+            oi = oe - 1;
             break;
         }
         case OP_FORCE: {
-            const int j = op.slice, w = op.worker;
+            const int j = op.slice, n = op.count, w = op.worker;
             if (w == 0 && c->NG > 1 && !(c->rank == 0 && op.cycle == 0)) {
-                const int need = std::min(j + 1, ns - 1);
+                const int need = std::min(j + n, ns - 1);   // right neighbour of the block
                 CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[need], 0));
             }
             cudaEvent_t t0 = nullptr, t1 = nullptr;
+            // the previous per-atom energy records of this worker must be reduced first
+            if (c->T.pipe) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_energy[w], 0));
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
             c->stats.kernel_launches +=
-                force_launch(c->g, c->T, in_of(w), c->stg[w], c->outb[w].cnt, j, 1,
+                force_launch(c->g, c->T, in_of(w), c->stg[w], c->outb[w].cnt, j, n,
                              c->e_dev + (size_t)op.t_rel * ns, c->partials, c->tickets, c->err_dev, c->cs);
             c->stats.force_launches++;
             if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_FORCE, {t0, t1}}); }
+            if (c->T.pipe) {  // per-slice energy reduction off the critical path
+                CUDA_TRY(c, cudaEventRecord(c->ev_force[w], c->cs));
+                CUDA_TRY(c, cudaStreamWaitEvent(c->es, c->ev_force[w], 0));
+                energy_launch(c->g, c->stg[w], j, n, c->e_dev + (size_t)op.t_rel * ns, c->es);
+                CUDA_TRY(c, cudaEventRecord(c->ev_energy[w], c->es));
+                c->stats.kernel_launches++;
+            }
             if (w == 0 && c->NG > 1) {
-                if (j > 0) CUDA_TRY(c, cudaEventRecord(c->ev_free[j - 1], c->cs));
-                if (j == ns - 1) CUDA_TRY(c, cudaEventRecord(c->ev_free[j], c->cs));
+                // slot s is last read by the unit of slice s+1
+                for (int sl = std::max(j - 1, 0); sl <= j + n - 2; sl++)
+                    CUDA_TRY(c, cudaEventRecord(c->ev_free[sl], c->cs));
+                if (j + n == ns) CUDA_TRY(c, cudaEventRecord(c->ev_free[ns - 1], c->cs));
             }
             break;
         }
         case OP_PASS: {
-            const int j = op.slice, w = op.worker;
+            const int j = op.slice, n = op.count, w = op.worker;
             if (w == 0 && c->NG > 1 && !(c->rank == 0 && op.cycle == 0))
-                CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[j], 0));
-            if (w == W - 1 && c->NG > 1 && sent[j]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[j], 0));
+                CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[j + n - 1], 0));
+            if (w == W - 1 && c->NG > 1)
+                for (int sl = j; sl < j + n; sl++)
+                    if (sent[sl]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[sl], 0));
             BufView& src = in_of(w);
             BufView& dst = c->outb[w];
             if (src.base != dst.base)
-                CUDA_TRY(c, cudaMemcpyAsync(dst.base + (size_t)j * sb, src.base + (size_t)j * sb, sb,
+                CUDA_TRY(c, cudaMemcpyAsync(dst.base + (size_t)j * sb, src.base + (size_t)j * sb, sb * n,
                                             cudaMemcpyDeviceToDevice, c->cs));
-            if (w == 0 && c->NG > 1) CUDA_TRY(c, cudaEventRecord(c->ev_free[j], c->cs));
-            if (w == W - 1 && c->NG > 1) CUDA_TRY(c, cudaEventRecord(c->ev_bin[j], c->cs));
+            for (int sl = j; sl < j + n; sl++) {
+                if (w == 0 && c->NG > 1) CUDA_TRY(c, cudaEventRecord(c->ev_free[sl], c->cs));
+                if (w == W - 1 && c->NG > 1) CUDA_TRY(c, cudaEventRecord(c->ev_bin[sl], c->cs));
+            }
             break;
         }
         case OP_BIN: {
-            const int m = op.slice, w = op.worker;
-            if (w == W - 1 && c->NG > 1 && sent[m]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[m], 0));
+            const int m = op.slice, n = op.count, w = op.worker;
+            if (w == W - 1 && c->NG > 1)
+                for (int sl = m; sl < m + n; sl++)
+                    if (sent[sl]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[sl], 0));
             cudaEvent_t t0 = nullptr, t1 = nullptr;
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
-            const int s0 = std::max(m - 1, 0), s1 = std::min(m + 1, ns - 1);
+            const int s0 = std::max(m - 1, 0), s1 = std::min(m + n, ns - 1);
             BufView& ob = c->outb[w];
-            bin_scan_launch(c->g, ob, m, 1, c->err_dev, c->cs);
-            bin_place_launch(c->g, ob, c->stg[w], s0, s1 - s0 + 1, 0, m, 1, c->err_dev, c->cs);
-            bin_gather_launch(c->g, ob, c->stg[w], m, 1, c->err_dev, c->cs);
+            bin_scan_launch(c->g, ob, m, n, c->err_dev, c->cs);
+            bin_place_launch(c->g, ob, c->stg[w], s0, s1 - s0 + 1, 0, m, n, c->err_dev, c->cs);
+            bin_gather_launch(c->g, ob, c->stg[w], m, n, c->err_dev, c->cs);
             c->stats.kernel_launches += 3;
             if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_BIN, {t0, t1}}); }
-            if (w == W - 1 && c->NG > 1) CUDA_TRY(c, cudaEventRecord(c->ev_bin[m], c->cs));
+            if (w == W - 1 && c->NG > 1)
+                for (int sl = m; sl < m + n; sl++) CUDA_TRY(c, cudaEventRecord(c->ev_bin[sl], c->cs));
             break;
         }
         case OP_SEND: {
-            if (c->NG == 1) break;  // ring of one: the last worker wrote into the input buffer
-            const int m = op.slice;
-            CUDA_TRY(c, cudaStreamWaitEvent(c->ss, c->ev_bin[m], 0));
+            size_t oe = oi;
+            while (oe < nops && P.ops[oe].kind == OP_SEND && P.ops[oe].stage == op.stage) oe++;
+            if (c->NG == 1) { oi = oe - 1; break; }  // ring of one: written into the input buffer
+            for (size_t q = oi; q < oe; q++)
+                CUDA_TRY(c, cudaStreamWaitEvent(c->ss, c->ev_bin[P.ops[q].slice], 0));
             cudaEvent_t t0 = nullptr, t1 = nullptr;
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->ss); }
-            ncclResult_t r = api.Send(c->outb[W - 1].base + (size_t)m * sb, sb, ncclChar, 1,
-                                      c->send_comm, c->ss);
-            if (r != ncclSuccess) return fail(c, DSEA_EPEER, "ncclSend: %s", api.GetErrorString(r));
+            api.GroupStart();
+            for (size_t q = oi; q < oe; q++) {
+                ncclResult_t r = api.Send(c->outb[W - 1].base + (size_t)P.ops[q].slice * sb, sb, ncclChar, 1,
+                                          c->send_comm, c->ss);
+                if (r != ncclSuccess) { api.GroupEnd(); return fail(c, DSEA_EPEER, "ncclSend: %s", api.GetErrorString(r)); }
+            }
+            ncclResult_t r = api.GroupEnd();
+            if (r != ncclSuccess) return fail(c, DSEA_EPEER, "ncclGroupEnd (send): %s", api.GetErrorString(r));
             if (c->timing) { cudaEventRecord(t1, c->ss); c->tpairs.push_back({TK_SEND, {t0, t1}}); }
-            CUDA_TRY(c, cudaEventRecord(c->ev_send[m], c->ss));
-            sent[m] = 1;
-            c->stats.hop_bytes += (int64_t)sb;
+            for (size_t q = oi; q < oe; q++) {
+                CUDA_TRY(c, cudaEventRecord(c->ev_send[P.ops[q].slice], c->ss));
+                sent[P.ops[q].slice] = 1;
+                c->stats.hop_bytes += (int64_t)sb;
+            }
+            oi = oe - 1;
             break;
         }
         }
@@ -594,8 +665,16 @@ dsea_status run_fused(dsea_ctx* c, int64_t n_steps)
     for (int64_t t = 0; t < n_steps; t++) {
         cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr;
         if (c->timing) { t0 = tev(c); t1 = tev(c); t2 = tev(c); cudaEventRecord(t0, c->cs); }
-        const int nl = force_launch(c->g, c->T, c->inb, c->stg[0], c->inb.cnt, 0, ns,
-                                    c->e_dev + (size_t)t * ns, c->partials, c->tickets, c->err_dev, c->cs);
+        if (c->T.pipe) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_energy[0], 0));
+        int nl = force_launch(c->g, c->T, c->inb, c->stg[0], c->inb.cnt, 0, ns,
+                              c->e_dev + (size_t)t * ns, c->partials, c->tickets, c->err_dev, c->cs);
+        if (c->T.pipe) {
+            CUDA_TRY(c, cudaEventRecord(c->ev_force[0], c->cs));
+            CUDA_TRY(c, cudaStreamWaitEvent(c->es, c->ev_force[0], 0));
+            energy_launch(c->g, c->stg[0], 0, ns, c->e_dev + (size_t)t * ns, c->es);
+            CUDA_TRY(c, cudaEventRecord(c->ev_energy[0], c->es));
+            nl++;
+        }
         if (c->timing) cudaEventRecord(t1, c->cs);
         bin_scan_launch(c->g, c->inb, 0, ns, c->err_dev, c->cs);
         bin_place_launch(c->g, c->inb, c->stg[0], 0, ns, 0, 0, ns, c->err_dev, c->cs);
@@ -674,9 +753,25 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     std::string why;
     dsea_status s = compute_geometry(&c->box, sp, &geo, &why);
     if (s) return fail(c, s, "%s", why.c_str());
-    if (mode == DSEA_MODE_STAGED && sp->n_gpus == 1 && geo.n_slices < 2 + 2 * sp->workers_per_gpu)
-        return fail(c, DSEA_EGEOM, "a ring of one with W = %d workers needs N_S >= %d slices (Eq. 1), got %d",
-                    sp->workers_per_gpu, 2 + 2 * sp->workers_per_gpu, geo.n_slices);
+    // slices per stage (block size B): enough atoms per launch to fill a B200, but
+    // keep >= N_GPU*(2+W) blocks per super-cycle so the ring stays busy (Eq. (1))
+    int B = sp->slices_per_stage;
+    if (B < 0) return fail(c, DSEA_EINVAL, "slices_per_stage < 0");
+    if (B == 0) {
+        const double per_slice = (double)geo.n_atoms / geo.n_slices;
+        B = std::max(1, (int)std::ceil(1.0e6 / per_slice));
+        const int depth = sp->n_gpus * (2 + sp->workers_per_gpu);
+        while (B > 1 && (geo.n_slices + B - 1) / B < depth) B--;
+        if (mode == DSEA_MODE_FUSED) B = 1;
+    }
+    B = std::min(B, std::max(1, geo.n_slices - 2));
+    if (mode == DSEA_MODE_STAGED && sp->n_gpus == 1) {
+        const int nblk = (geo.n_slices + B - 1) / B;
+        const bool ok = B == 1 ? geo.n_slices >= 2 + 2 * sp->workers_per_gpu : nblk >= 2 + sp->workers_per_gpu;
+        if (!ok)
+            return fail(c, DSEA_EGEOM, "a ring of one with W = %d workers and %d slices per stage needs more "
+                        "slices (N_S = %d; Eq. (1))", sp->workers_per_gpu, B, geo.n_slices);
+    }
 
     // keep the current state (host mirror of the device or the host arrays)
     std::vector<double> xyz, v, f;
@@ -694,6 +789,7 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     c->mode = mode;
     c->geo = geo;
     c->W = sp->workers_per_gpu;
+    c->B = B;
     c->NG = sp->n_gpus;
     c->rank = sp->rank;
     c->device = sp->device;
@@ -721,12 +817,16 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, sp->device));
     const double mean_per_cell = (double)c->N / ((double)g.ns * g.ncell);
     c->T = choose_tiling(g, mean_per_cell, optin);
-    if (force_kernel_attr(c->T) != 0)
-        return fail(c, DSEA_ECUDA, "cannot set %zu bytes of dynamic shared memory", c->T.smem);
+    const int per_sm = force_kernel_attr(c->T);
+    if (per_sm < 1) return fail(c, DSEA_ECUDA, "cannot set %zu bytes of dynamic shared memory", c->T.smem);
+    int sms = 0;
+    CUDA_TRY(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sp->device));
+    c->T.grid = sms * per_sm;
 
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->ss, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->rs, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->es, cudaStreamNonBlocking));
     c->sliced = true;
 
     // buffers: input buffer + one output buffer per worker; the last worker of a ring
@@ -745,7 +845,18 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     if ((s = dalloc(c, &c->tickets, (size_t)g.ns))) return s;
     CUDA_TRY(c, cudaMemset(c->tickets, 0, sizeof(unsigned) * g.ns));
     if ((s = dalloc(c, &c->err_dev, 1))) return s;
+    if ((s = dalloc(c, &c->tile_ctr, 1))) return s;
+    CUDA_TRY(c, cudaMemset(c->tile_ctr, 0, sizeof(unsigned long long)));
+    c->tile_ctr_base = 0;
+    c->T.ctr = c->tile_ctr;
+    c->T.ctr_base = &c->tile_ctr_base;
     CUDA_TRY(c, cudaMemset(c->err_dev, 0, sizeof(DevErr)));
+    c->ev_force.resize(c->W);
+    c->ev_energy.resize(c->W);
+    for (int w = 0; w < c->W; w++) {
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_force[w], cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_energy[w], cudaEventDisableTiming));
+    }
     for (auto* v : {&c->ev_recv, &c->ev_free, &c->ev_bin, &c->ev_send}) {
         v->resize(g.ns);
         for (int j = 0; j < g.ns; j++) CUDA_TRY(c, cudaEventCreateWithFlags(&(*v)[j], cudaEventDisableTiming));
@@ -823,6 +934,7 @@ dsea_status dsea_step(dsea_ctx* c, int64_t n_steps)
     CUDA_TRY(c, cudaStreamSynchronize(c->cs));
     CUDA_TRY(c, cudaStreamSynchronize(c->ss));
     CUDA_TRY(c, cudaStreamSynchronize(c->rs));
+    CUDA_TRY(c, cudaStreamSynchronize(c->es));
     CUDA_TRY(c, cudaGetLastError());
     if ((s = check_dev_err(c))) return s;
 
@@ -960,7 +1072,7 @@ dsea_status dsea_schedule(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_
     if (!n_rows || n_slices < 1 || n_gpus < 1 || rank < 0 || rank >= n_gpus || W < 1 || n_cycles < 0)
         return DSEA_EINVAL;
     const int64_t n_steps = (int64_t)n_cycles * n_gpus * W;
-    const Plan P = build_plan(n_slices, n_gpus, rank, W, n_steps);
+    const Plan P = build_plan(n_slices, n_gpus, rank, W, n_steps, 1);
     // one row per (stage, worker) doing something; recv rows carry worker -1
     std::vector<std::array<int32_t, 8>> out;
     auto row_for = [&](int stage, int worker) -> std::array<int32_t, 8>& {

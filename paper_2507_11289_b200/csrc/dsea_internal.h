@@ -82,6 +82,9 @@ struct Tiling {
     int maxh;        // per-lane hit-list capacity
     size_t smem;     // dynamic shared memory bytes
     bool pipe;       // persistent pipelined kernel (default) or the one-tile-per-CTA kernel
+    int grid;        // persistent grid = SMs x resident CTAs per SM
+    unsigned long long* ctr;       // device: dynamic tile counter of this context
+    unsigned long long* ctr_base;  // host: counter value at the next launch
 };
 
 // Energy record of one (slice, timestep) unit.
@@ -105,6 +108,7 @@ size_t pipe_smem_bytes(int smax, int maxh);
 int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t* out_cnt,
                  int j0, int nj, UnitEnergy* e_out, double4* partials, unsigned* tickets,
                  DevErr* err, cudaStream_t s);
+void energy_launch(const Geo& g, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s);
 void bin_scan_launch(const Geo& g, BufView out, int m0, int nm, DevErr* err, cudaStream_t s);
 void bin_place_launch(const Geo& g, BufView out, StgView stg, int s0, int nsrc, int flat_count,
                       int m0, int nm, DevErr* err, cudaStream_t s);

@@ -537,7 +537,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) 
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
         if (ok) return;
-        __nanosleep(256);
+        __nanosleep(1000);
     }
 }
 
@@ -567,7 +567,8 @@ size_t pipe_smem_bytes(int smax, int maxh)
 
 __global__ void __launch_bounds__(PIPE_THREADS, 2)
 k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt, int j0, int nj,
-             DevErr* __restrict__ err)
+             DevErr* __restrict__ err, unsigned long long* __restrict__ tile_ctr,
+             unsigned long long ctr_base)
 {
     constexpr int IL = 16;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -594,10 +595,17 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
         // ============================ producer (2 warps) ============================
         // warp P0 builds each tile's piece table; both producer warps stage it.
         const int pw = warp - PIPE_CWARPS, pl = pw * 32 + lane;
-        __shared__ int sh_he, sh_ok, sh_total, sh_main_start, sh_main_dst;
+        __shared__ int sh_he, sh_ok, sh_total, sh_main_start, sh_main_dst, sh_tile;
         int it = 0;
         const long long ntiles = (long long)nj * T.tiles;
-        for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (;;) {
+            // dynamic tile scheduling: CTAs that start late (SMs busy with other work,
+            // e.g. NCCL) simply take fewer tiles
+            if (pl == 0) sh_tile = (int)(atomicAdd(tile_ctr, 1ull) - ctr_base);
+            asm volatile("bar.sync 1, 64;" ::: "memory");
+            const long long t = sh_tile;
+            asm volatile("bar.sync 1, 64;" ::: "memory");
+            if (t >= ntiles) break;
             const int j = j0 + (int)(t / T.tiles);
             const int tile = (int)(t % T.tiles);
             const int tt = tile % T.nzt;
@@ -761,7 +769,7 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
     const float rc2s = g.rc2_screen;
     const double rc2 = g.rc2;
     const int maxh = T.maxh;
-    constexpr int SEG_PAIRS = 32;
+    constexpr int SEG_PAIRS = 16;           // pairs per lane group per segment
     constexpr int seg_need = SEG_PAIRS;     // max appends per lane per segment (JPAR = 2)
     const float2 m1 = make_float2(-1.f, -1.f);
     int it = 0;
@@ -1127,7 +1135,8 @@ static size_t force_smem_bytes(int smax, int jpar, int maxh)
            (size_t)(smax / 16 + 64 + 1) * sizeof(double4) + (size_t)maxh * FORCE_THREADS * sizeof(uint16_t);
 }
 
-static int pipe_grid = 0;  // persistent grid: SMs x resident CTAs (set by force_kernel_attr)
+
+static size_t pipe_smem_attr = 0;    // largest dynamic smem set on k_force_pipe so far
 
 static double env_num(const char* name, double dflt)
 {
@@ -1170,16 +1179,18 @@ Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
 int force_kernel_attr(const Tiling& T)
 {
     if (T.pipe) {
-        cudaError_t e = cudaFuncSetAttribute(k_force_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)T.smem);
-        if (e != cudaSuccess) return -1;
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // the attribute is process-wide: keep the largest request of any context
+        if (T.smem > pipe_smem_attr) {
+            cudaError_t e = cudaFuncSetAttribute(k_force_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)T.smem);
+            if (e != cudaSuccess) return -1;
+            pipe_smem_attr = T.smem;
+        }
+        int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force_pipe, PIPE_THREADS, T.smem);
         if (per_sm < 1) return -1;
-        pipe_grid = sms * per_sm;
-        return 0;
+
+        return per_sm;
     }
     cudaError_t e = T.jpar == 4
         ? cudaFuncSetAttribute(k_force<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem)
@@ -1192,9 +1203,12 @@ int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t
                  cudaStream_t s)
 {
     if (T.pipe) {
-        k_force_pipe<<<pipe_grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err);
-        k_energy<<<nj, ENERGY_THREADS, 0, s>>>(g, stg, j0, e_out);
-        return 2;
+        // the tile counter is never reset: each launch consumes exactly ntiles + grid
+        // increments, so the host tracks the base of every launch
+        k_force_pipe<<<T.grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err,
+                                                          T.ctr, *T.ctr_base);
+        *T.ctr_base += (unsigned long long)nj * T.tiles + T.grid;
+        return 1;
     }
     dim3 grid(T.tiles, nj);
     if (T.jpar == 4)
@@ -1204,6 +1218,11 @@ int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t
         k_force<2><<<grid, FORCE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, e_out, partials,
                                                        tickets, err);
     return 1;
+}
+
+void energy_launch(const Geo& g, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s)
+{
+    k_energy<<<nj, ENERGY_THREADS, 0, s>>>(g, stg, j0, e_out);
 }
 
 void bin_scan_launch(const Geo& g, BufView out, int m0, int nm, DevErr* err, cudaStream_t s)

@@ -47,7 +47,7 @@ class dsea_slice_params(ctypes.Structure):
     _fields_ = [("n_slices", ctypes.c_int32), ("cells_per_slice_x", ctypes.c_int32),
                 ("n_gpus", ctypes.c_int32), ("rank", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("workers_per_gpu", ctypes.c_int32), ("mode", ctypes.c_int32),
-                ("capacity_factor", ctypes.c_double)]
+                ("slices_per_stage", ctypes.c_int32), ("capacity_factor", ctypes.c_double)]
 
 
 class dsea_geometry(ctypes.Structure):
@@ -143,9 +143,9 @@ def dsea_init(nx, ny, nz, rho, rc, dt=0.0018, T0=1.0, seed=11289):
 
 
 def dsea_slice(ctx, n_slices=0, cells_per_slice_x=1, n_gpus=1, rank=0, device=0,
-               workers_per_gpu=1, mode=DSEA_MODE_AUTO, capacity_factor=0.0):
+               workers_per_gpu=1, mode=DSEA_MODE_AUTO, capacity_factor=0.0, slices_per_stage=0):
     sp = dsea_slice_params(n_slices, cells_per_slice_x, n_gpus, rank, device, workers_per_gpu,
-                           mode, capacity_factor)
+                           mode, slices_per_stage, capacity_factor)
     _check(ctx, lib.dsea_slice(ctx, ctypes.byref(sp)))
 
 
@@ -248,7 +248,7 @@ def dsea_reset_stats(ctx):
 def dsea_geometry_compute(nx, ny, nz, rho, rc, n_slices=0, cells_per_slice_x=1, workers_per_gpu=1,
                           capacity_factor=0.0):
     box = dsea_box_params(nx, ny, nz, rho, rc, 0.0018, 1.0, 0)
-    sp = dsea_slice_params(n_slices, cells_per_slice_x, 1, 0, 0, workers_per_gpu, 0, capacity_factor)
+    sp = dsea_slice_params(n_slices, cells_per_slice_x, 1, 0, 0, workers_per_gpu, 0, 1, capacity_factor)
     g = dsea_geometry()
     st = lib.dsea_geometry_compute(ctypes.byref(box), ctypes.byref(sp), ctypes.byref(g))
     return st, g

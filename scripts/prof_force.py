@@ -6,7 +6,8 @@ from paper_2507_11289_b200 import dsea as D
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 e = D.Engine(D.Box(cfg.nx, cfg.ny, cfg.nz, cfg.rho, cfg.rc, cfg.dt, cfg.T0, cfg.seed))
-e.slice(n_slices=cfg.n_slices, cells_per_slice_x=cfg.cells_per_slice_x)
+mode = int(os.environ.get("PROF_MODE", "0")); B = int(os.environ.get("PROF_B", "0"))
+e.slice(n_slices=cfg.n_slices, cells_per_slice_x=cfg.cells_per_slice_x, mode=mode, slices_per_stage=B)
 D.dsea_set_timing(e.ctx, True)
 e.step(steps)
 st = e.stats()

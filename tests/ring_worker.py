@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--calls", type=int, default=1)
+    ap.add_argument("--block", type=int, default=0, help="slices per stage (0 = auto)")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     rank = int(os.environ["RANK"])
@@ -42,7 +43,7 @@ def main():
     c = CONFIGS[a.config]
     e = D.Engine(D.Box(c.nx, c.ny, c.nz, c.rho, c.rc, c.dt, c.T0, c.seed))
     e.slice(n_slices=c.n_slices, cells_per_slice_x=c.cells_per_slice_x, n_gpus=world, rank=rank,
-            device=local, workers_per_gpu=a.workers)
+            device=local, workers_per_gpu=a.workers, slices_per_stage=a.block)
     _log(rank, "sliced")
     ids = [b"".join(D.dsea_ring_unique_id() for _ in range(world))] if rank == 0 else [None]
     dist.broadcast_object_list(ids, src=0)

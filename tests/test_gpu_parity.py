@@ -152,14 +152,15 @@ def test_cutoff_and_slice_thickness_variants(rc, c_per, ns):
     _cells_exact(e, c)
 
 
-@pytest.mark.parametrize("W,mode", [(1, D.DSEA_MODE_STAGED), (2, D.DSEA_MODE_STAGED), (3, D.DSEA_MODE_STAGED)])
-def test_ring_of_one_bitwise_equals_fused(W, mode):
-    """The stage schedule (Table 1, W workers sequential on one GPU) and the
-    fused whole-domain pass compute the same unit results: bitwise equal states
-    after 7 steps (7 is not a multiple of W = 2, 3: pass-through workers, Q15)."""
+@pytest.mark.parametrize("W,B", [(1, 1), (2, 1), (3, 1), (1, 3), (2, 4), (3, 2)])
+def test_ring_of_one_bitwise_equals_fused(W, B):
+    """The stage schedule (Table 1 for B = 1; B slices per stage otherwise; W workers
+    sequential on one GPU) and the fused whole-domain pass compute the same
+    unit results: bitwise equal states after 7 steps (7 is not a multiple of W = 2, 3:
+    pass-through workers, Q15)."""
     ref, c = _engine("P8")
     ref.step(7)
-    e, _ = _engine("P8", workers_per_gpu=W, mode=mode)
+    e, _ = _engine("P8", workers_per_gpu=W, mode=D.DSEA_MODE_STAGED, slices_per_stage=B)
     e.step(7)
     assert np.array_equal(e.positions(), ref.positions())
     assert np.array_equal(e.velocities(), ref.velocities())
