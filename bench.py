@@ -199,6 +199,9 @@ def main():
     ap.add_argument("--equil", type=int, default=200, help="untimed melting timesteps before warm-up")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--hop", default="peer", choices=["peer", "nccl"],
+                    help="ring hop: fused NVLink remote stores (peer) or NCCL send/recv")
+    ap.add_argument("--block", type=int, default=0, help="slices per stage (0 = auto)")
     args = ap.parse_args()
 
     from paper_2507_11289_b200 import CONFIGS
@@ -224,11 +227,9 @@ def main():
     W = args.workers
     e = D.Engine(D.Box(cfg.nx, cfg.ny, cfg.nz, cfg.rho, cfg.rc, cfg.dt, cfg.T0, cfg.seed))
     e.slice(n_slices=cfg.n_slices, cells_per_slice_x=cfg.cells_per_slice_x, n_gpus=world, rank=rank,
-            device=local_rank, workers_per_gpu=W)
+            device=local_rank, workers_per_gpu=W, slices_per_stage=args.block)
     if world > 1:
-        ids = [b"".join(D.dsea_ring_unique_id() for _ in range(world))] if rank == 0 else [None]
-        dist.broadcast_object_list(ids, src=0)
-        D.dsea_ring_connect(e.ctx, ids[0], world)
+        D.ring_connect(e.ctx, rank, world, args.hop)
     geo = e.geometry
     nw = world * W
 
@@ -327,7 +328,7 @@ def main():
                        "workers_per_gpu": W, "timesteps_per_step": nw,
                        "mode": "fused" if world == 1 and W == 1 else "staged-ring",
                        "l2": "inputs larger than L2 (state %.2f GB)" % (atoms * 76 / 1e9),
-                       "parallelism": f"ring{world}"},
+                       "parallelism": f"ring{world}", "ring_hop": args.hop if world > 1 else None},
             "roofline": {"bound": "alu", "achieved": fp64_achieved, "peak": fp64_peak,
                          "unit": "TFLOP/s", "frac": fp64_achieved / fp64_peak,
                          "traffic": (None if traffic_pa is None else traffic_pa * atoms_per_launch),
@@ -346,6 +347,9 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        D.ring_disconnect(e.ctx, world)
     e.close()
     if dist is not None:
         dist.barrier()

@@ -149,6 +149,26 @@ dsea_status dsea_ring_connect(dsea_ctx *ctx, const void *ids, int32_t n_ids);
 /* Write one fresh 128-byte ncclUniqueId into out (out_bytes >= 128). */
 dsea_status dsea_ring_unique_id(void *out, size_t out_bytes);
 
+/* Peer backend (default for bench.py).  The ring hop of P:118-119 is fused into the
+ * finalisation of the last worker on each GPU: its bin kernels write the finished
+ * slices straight into the successor GPU's input slots over NVLink (CUDA IPC
+ * mapping), and arrival / release counts travel through two small flag arrays
+ * (receivers wait on local flags with stream memory operations).  No copy, no
+ * NCCL kernel on the data path.
+ * dsea_ring_export writes this rank's IPC handles (input buffer, flag arrays) into
+ * out (cap >= *len; out = NULL queries *len).  dsea_ring_connect_peer takes the
+ * n_blobs = n_gpus blobs of all ranks, concatenated in rank order (each blob_bytes
+ * long), maps the successor's input buffer and flags and the predecessor's release
+ * flags.  Collective: every rank calls it, then the caller must barrier before the
+ * first dsea_step.  Exclusive with dsea_ring_connect on a context. */
+dsea_status dsea_ring_export(dsea_ctx *ctx, void *out, size_t cap, size_t *len);
+dsea_status dsea_ring_connect_peer(dsea_ctx *ctx, const void *blobs, size_t blob_bytes, int32_t n_blobs);
+
+/* Leave the ring: close the peer mappings (or NCCL links).  Collective; call it on
+ * every rank and barrier before dsea_destroy, because a rank must not free memory
+ * that its neighbour still maps.  Idempotent. */
+dsea_status dsea_ring_disconnect(dsea_ctx *ctx);
+
 /* Advance the system n_steps timesteps (n_steps >= 0) by streaming the slices
  * through the ring of workers: ceil(n_steps / N_w) super-cycles of N_w =
  * N_GPU*W timesteps, the trailing workers of a partial last

@@ -68,6 +68,29 @@ NcclApi& nccl()
     return api;
 }
 
+// cuStreamWaitValue32 through the runtime's driver entry point (no libcuda link)
+typedef int (*PFN_waitValue32)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+PFN_waitValue32 wait_value32()
+{
+    static PFN_waitValue32 f = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            f = reinterpret_cast<PFN_waitValue32>(p);
+    }
+    return f;
+}
+
+struct PeerBlob {
+    int32_t magic, rank, ns, pad;
+    cudaIpcMemHandle_t in, arr, rel;
+};
+constexpr int32_t PEER_MAGIC = 0x44534541;  // "DSEA"
+
 // ------------------------------------------------------------------------------
 // Stage schedule (Table 1 generalised).  The slices of a super-cycle are grouped in
 // blocks of B consecutive slices (B = 1 is the paper's schedule); flat blocks
@@ -177,7 +200,7 @@ struct dsea_ctx {
     int mode = DSEA_MODE_FUSED;
     int W = 1, NG = 1, rank = 0, device = 0, B = 1;
 
-    cudaStream_t cs = nullptr, ss = nullptr, rs = nullptr, es = nullptr;  // compute, send, recv, energy
+    cudaStream_t cs = nullptr, ss = nullptr, rs = nullptr, es = nullptr, bs = nullptr;  // compute, send, recv, energy, remote bin
     BufView inb{};
     std::vector<BufView> outb;
     std::vector<StgView> stg;
@@ -191,9 +214,22 @@ struct dsea_ctx {
     unsigned long long tile_ctr_base = 0;
     std::vector<cudaEvent_t> ev_recv, ev_free, ev_bin, ev_send;
     std::vector<cudaEvent_t> ev_force, ev_energy;   // per worker: force done / energies done
+    std::vector<cudaEvent_t> ev_binblk;             // per block: last remote bin run done
+    cudaEvent_t ev_cs = nullptr;                    // compute-stream point for the bin stream
 
     bool connected = false;
     ncclComm_t send_comm = nullptr, recv_comm = nullptr;
+    // peer backend: the last worker's bins write the finished slices straight into the
+    // successor's input slots (CUDA IPC mapping over NVLink); arrival / release counts
+    // travel through flag arrays (waits on local flags, writes by a signal kernel)
+    bool peer = false;
+    uint32_t* arr_dev = nullptr;        // [ns] local: arrivals into my input slots
+    uint32_t* rel_dev = nullptr;        // [ns] local: releases of my successor's slots
+    char* succ_in_base = nullptr;       // mapped successor input buffer
+    uint32_t* succ_arr = nullptr;       // mapped successor arrival flags
+    uint32_t* pred_rel = nullptr;       // mapped predecessor release flags
+    std::vector<uint32_t> wr_cnt, exp_arr, rel_cnt;
+    char* own_outb_last = nullptr;      // locally allocated last output buffer (unused when peer)
 
     // host mirror of the device state (rank 0), valid until the next mutation
     std::vector<char> mirror;
@@ -333,9 +369,28 @@ void host_velocities(int64_t n, uint64_t seed, double T0, double* v)
     for (int64_t i = 0; i < 3 * n; i++) v[i] *= f;
 }
 
+void disconnect(dsea_ctx* c)
+{
+    if (c->sliced) cudaSetDevice(c->device);
+    if (c->peer) {
+        cudaDeviceSynchronize();
+        if (c->succ_in_base) cudaIpcCloseMemHandle(c->succ_in_base);
+        if (c->succ_arr) cudaIpcCloseMemHandle(c->succ_arr);
+        if (c->pred_rel) cudaIpcCloseMemHandle(c->pred_rel);
+        c->succ_in_base = nullptr; c->succ_arr = nullptr; c->pred_rel = nullptr;
+        c->peer = false;
+        if (!c->outb.empty() && c->outb.back().remote) {
+            c->outb.back().base = c->own_outb_last;
+            c->outb.back().remote = 0;
+        }
+        c->connected = false;
+    }
+}
+
 void free_device(dsea_ctx* c)
 {
     if (c->sliced) cudaSetDevice(c->device);
+    disconnect(c);
     if (c->connected) {
         if (nccl().ok) {
             // ncclCommDestroy finalizes collectively: destroy the two link
@@ -363,6 +418,12 @@ void free_device(dsea_ctx* c)
     if (c->ss) cudaStreamDestroy(c->ss);
     if (c->rs) cudaStreamDestroy(c->rs);
     if (c->es) cudaStreamDestroy(c->es);
+    if (c->bs) cudaStreamDestroy(c->bs);
+    for (cudaEvent_t e : c->ev_binblk) cudaEventDestroy(e);
+    c->ev_binblk.clear();
+    if (c->ev_cs) cudaEventDestroy(c->ev_cs);
+    c->ev_cs = nullptr;
+    c->bs = nullptr;
     for (cudaEvent_t e : c->ev_force) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_energy) cudaEventDestroy(e);
     c->ev_force.clear(); c->ev_energy.clear();
@@ -545,6 +606,10 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
         const Op& op = P.ops[oi];
         switch (op.kind) {
         case OP_RECV: {
+            if (c->peer) {  // data arrives by remote stores; just count the expected arrival
+                c->exp_arr[op.slice]++;
+                break;
+            }
             // all receives of this stage in one NCCL group (matched by order with the
             // predecessor's sends, one message per slice)
             size_t oe = oi;
@@ -567,11 +632,22 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             const int j = op.slice, n = op.count, w = op.worker;
             if (w == 0 && c->NG > 1 && !(c->rank == 0 && op.cycle == 0)) {
                 const int need = std::min(j + n, ns - 1);   // right neighbour of the block
-                CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[need], 0));
+                if (c->peer) {
+                    if (wait_value32()(c->cs, (unsigned long long)(c->arr_dev + need), c->exp_arr[need], 0))
+                        return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (arrival) failed");
+                } else {
+                    CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[need], 0));
+                }
             }
             cudaEvent_t t0 = nullptr, t1 = nullptr;
             // the previous per-atom energy records of this worker must be reduced first
             if (c->T.pipe) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_energy[w], 0));
+            if (c->peer && w == W - 1) {
+                // staging of this block and the arrival counters it adds to were last read
+                // by the remote bin runs of blocks c and c+1 one super-cycle ago
+                const int nblk = (ns + c->B - 1) / c->B;
+                CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_binblk[(j / c->B + 1) % nblk], 0));
+            }
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
             c->stats.kernel_launches +=
                 force_launch(c->g, c->T, in_of(w), c->stg[w], c->outb[w].cnt, j, n,
@@ -587,52 +663,115 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             }
             if (w == 0 && c->NG > 1) {
                 // slot s is last read by the unit of slice s+1
-                for (int sl = std::max(j - 1, 0); sl <= j + n - 2; sl++)
-                    CUDA_TRY(c, cudaEventRecord(c->ev_free[sl], c->cs));
-                if (j + n == ns) CUDA_TRY(c, cudaEventRecord(c->ev_free[ns - 1], c->cs));
+                const int f0 = std::max(j - 1, 0), f1 = (j + n == ns) ? ns - 1 : j + n - 2;
+                if (c->peer) {
+                    if (f1 >= f0) {  // release the slots to the predecessor (one count per cycle)
+                        const uint32_t v = ++c->rel_cnt[f0];
+                        for (int sl = f0 + 1; sl <= f1; sl++) c->rel_cnt[sl] = v;
+                        signal_launch(c->pred_rel, f0, f1 - f0 + 1, v, c->cs);
+                        c->stats.kernel_launches++;
+                    }
+                } else {
+                    for (int sl = f0; sl <= f1; sl++) CUDA_TRY(c, cudaEventRecord(c->ev_free[sl], c->cs));
+                }
             }
             break;
         }
         case OP_PASS: {
             const int j = op.slice, n = op.count, w = op.worker;
-            if (w == 0 && c->NG > 1 && !(c->rank == 0 && op.cycle == 0))
-                CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[j + n - 1], 0));
-            if (w == W - 1 && c->NG > 1)
-                for (int sl = j; sl < j + n; sl++)
-                    if (sent[sl]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[sl], 0));
+            if (w == 0 && c->NG > 1 && !(c->rank == 0 && op.cycle == 0)) {
+                if (c->peer) {
+                    if (wait_value32()(c->cs, (unsigned long long)(c->arr_dev + j + n - 1), c->exp_arr[j + n - 1], 0))
+                        return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (arrival) failed");
+                } else {
+                    CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[j + n - 1], 0));
+                }
+            }
+            uint32_t wv = 0;
+            if (w == W - 1 && c->NG > 1) {
+                if (c->peer) {
+                    wv = ++c->wr_cnt[j];
+                    for (int sl = j + 1; sl < j + n; sl++) c->wr_cnt[sl] = wv;
+                    for (int sl = j; sl < j + n; sl++)
+                        if (wait_value32()(c->cs, (unsigned long long)(c->rel_dev + sl), wv, 0))
+                            return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (release) failed");
+                } else {
+                    for (int sl = j; sl < j + n; sl++)
+                        if (sent[sl]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[sl], 0));
+                }
+            }
             BufView& src = in_of(w);
             BufView& dst = c->outb[w];
             if (src.base != dst.base)
                 CUDA_TRY(c, cudaMemcpyAsync(dst.base + (size_t)j * sb, src.base + (size_t)j * sb, sb * n,
                                             cudaMemcpyDeviceToDevice, c->cs));
-            for (int sl = j; sl < j + n; sl++) {
-                if (w == 0 && c->NG > 1) CUDA_TRY(c, cudaEventRecord(c->ev_free[sl], c->cs));
-                if (w == W - 1 && c->NG > 1) CUDA_TRY(c, cudaEventRecord(c->ev_bin[sl], c->cs));
+            if (w == 0 && c->NG > 1) {
+                if (c->peer) {
+                    const uint32_t v = ++c->rel_cnt[j];
+                    for (int sl = j + 1; sl < j + n; sl++) c->rel_cnt[sl] = v;
+                    signal_launch(c->pred_rel, j, n, v, c->cs);
+                } else {
+                    for (int sl = j; sl < j + n; sl++) CUDA_TRY(c, cudaEventRecord(c->ev_free[sl], c->cs));
+                }
+            }
+            if (w == W - 1 && c->NG > 1) {
+                if (c->peer) signal_launch(c->succ_arr, j, n, wv, c->cs);
+                else for (int sl = j; sl < j + n; sl++) CUDA_TRY(c, cudaEventRecord(c->ev_bin[sl], c->cs));
             }
             break;
         }
         case OP_BIN: {
             const int m = op.slice, n = op.count, w = op.worker;
-            if (w == W - 1 && c->NG > 1)
-                for (int sl = m; sl < m + n; sl++)
-                    if (sent[sl]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[sl], 0));
+            uint32_t wv = 0;
+            // the last worker's bins write into the successor over NVLink: run them on
+            // their own stream so the transfer overlaps the next block's force pass
+            const bool remote = c->peer && w == W - 1;
+            cudaStream_t bst = remote ? c->bs : c->cs;
+            if (remote) {
+                CUDA_TRY(c, cudaEventRecord(c->ev_cs, c->cs));
+                CUDA_TRY(c, cudaStreamWaitEvent(c->bs, c->ev_cs, 0));
+            }
+            if (w == W - 1 && c->NG > 1) {
+                if (c->peer) {  // the successor must have released the previous occupants
+                    wv = ++c->wr_cnt[m];
+                    for (int sl = m + 1; sl < m + n; sl++) c->wr_cnt[sl] = wv;
+                    for (int sl = m; sl < m + n; sl++)
+                        if (wait_value32()(bst, (unsigned long long)(c->rel_dev + sl), wv, 0))
+                            return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (release) failed");
+                } else {
+                    for (int sl = m; sl < m + n; sl++)
+                        if (sent[sl]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[sl], 0));
+                }
+            }
             cudaEvent_t t0 = nullptr, t1 = nullptr;
-            if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
+            if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, bst); }
             const int s0 = std::max(m - 1, 0), s1 = std::min(m + n, ns - 1);
             BufView& ob = c->outb[w];
-            bin_scan_launch(c->g, ob, m, n, c->err_dev, c->cs);
-            bin_place_launch(c->g, ob, c->stg[w], s0, s1 - s0 + 1, 0, m, n, c->err_dev, c->cs);
-            bin_gather_launch(c->g, ob, c->stg[w], m, n, c->err_dev, c->cs);
+            bin_scan_launch(c->g, ob, m, n, c->err_dev, bst);
+            bin_place_launch(c->g, ob, c->stg[w], s0, s1 - s0 + 1, 0, m, n, c->err_dev, bst);
+            bin_gather_launch(c->g, ob, c->stg[w], m, n, c->err_dev, bst);
             c->stats.kernel_launches += 3;
-            if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_BIN, {t0, t1}}); }
-            if (w == W - 1 && c->NG > 1)
-                for (int sl = m; sl < m + n; sl++) CUDA_TRY(c, cudaEventRecord(c->ev_bin[sl], c->cs));
+            if (c->timing) { cudaEventRecord(t1, bst); c->tpairs.push_back({TK_BIN, {t0, t1}}); }
+            if (w == W - 1 && c->NG > 1) {
+                if (c->peer) {  // the slices are already in the successor's memory: publish
+                    signal_launch(c->succ_arr, m, n, wv, bst);
+                    c->stats.kernel_launches++;
+                    c->stats.hop_bytes += (int64_t)sb * n;
+                    // keyed by the block of this run's last slot: a force pass on block c
+                    // waits for the run covering slot (c+1)B, i.e. key c+1
+                    const int nblk = (ns + c->B - 1) / c->B;
+                    CUDA_TRY(c, cudaEventRecord(c->ev_binblk[((m + n - 1) / c->B) % nblk], bst));
+                } else {
+                    for (int sl = m; sl < m + n; sl++) CUDA_TRY(c, cudaEventRecord(c->ev_bin[sl], c->cs));
+                }
+            }
             break;
         }
         case OP_SEND: {
             size_t oe = oi;
             while (oe < nops && P.ops[oe].kind == OP_SEND && P.ops[oe].stage == op.stage) oe++;
-            if (c->NG == 1) { oi = oe - 1; break; }  // ring of one: written into the input buffer
+            // ring of one: written into the input buffer; peer: written into the successor
+            if (c->NG == 1 || c->peer) { oi = oe - 1; break; }
             for (size_t q = oi; q < oe; q++)
                 CUDA_TRY(c, cudaStreamWaitEvent(c->ss, c->ev_bin[P.ops[q].slice], 0));
             cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -655,6 +794,11 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             break;
         }
         }
+    }
+    if (c->peer && c->rank == 0) {  // the final super-cycle lands in rank 0's input buffer
+        for (int sl = 0; sl < ns; sl++)
+            if (wait_value32()(c->cs, (unsigned long long)(c->arr_dev + sl), c->exp_arr[sl], 0))
+                return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (final arrival) failed");
     }
     return DSEA_OK;
 }
@@ -827,6 +971,8 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->ss, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->rs, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->es, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->bs, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_cs, cudaEventDisableTiming));
     c->sliced = true;
 
     // buffers: input buffer + one output buffer per worker; the last worker of a ring
@@ -846,11 +992,20 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     CUDA_TRY(c, cudaMemset(c->tickets, 0, sizeof(unsigned) * g.ns));
     if ((s = dalloc(c, &c->err_dev, 1))) return s;
     if ((s = dalloc(c, &c->tile_ctr, 1))) return s;
+    if ((s = dalloc(c, &c->arr_dev, (size_t)g.ns))) return s;
+    if ((s = dalloc(c, &c->rel_dev, (size_t)g.ns))) return s;
+    CUDA_TRY(c, cudaMemset(c->arr_dev, 0, sizeof(uint32_t) * g.ns));
+    CUDA_TRY(c, cudaMemset(c->rel_dev, 0, sizeof(uint32_t) * g.ns));
     CUDA_TRY(c, cudaMemset(c->tile_ctr, 0, sizeof(unsigned long long)));
     c->tile_ctr_base = 0;
     c->T.ctr = c->tile_ctr;
     c->T.ctr_base = &c->tile_ctr_base;
     CUDA_TRY(c, cudaMemset(c->err_dev, 0, sizeof(DevErr)));
+    {
+        const int nblk = (g.ns + c->B - 1) / c->B;
+        c->ev_binblk.resize(nblk);
+        for (int k = 0; k < nblk; k++) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_binblk[k], cudaEventDisableTiming));
+    }
     c->ev_force.resize(c->W);
     c->ev_energy.resize(c->W);
     for (int w = 0; w < c->W; w++) {
@@ -905,6 +1060,83 @@ dsea_status dsea_ring_connect(dsea_ctx* c, const void* ids, int32_t n_ids)
     return DSEA_OK;
 }
 
+dsea_status dsea_ring_export(dsea_ctx* c, void* out, size_t cap, size_t* len)
+{
+    if (!c || !len) return DSEA_EINVAL;
+    *len = sizeof(PeerBlob);
+    if (!out) return DSEA_OK;
+    if (cap < sizeof(PeerBlob)) return fail(c, DSEA_EINVAL, "export buffer needs %zu bytes", sizeof(PeerBlob));
+    if (!c->sliced) return fail(c, DSEA_ESTATE, "dsea_ring_export before dsea_slice");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    PeerBlob b{};
+    b.magic = PEER_MAGIC;
+    b.rank = c->rank;
+    b.ns = c->g.ns;
+    CUDA_TRY(c, cudaIpcGetMemHandle(&b.in, c->inb.base));
+    CUDA_TRY(c, cudaIpcGetMemHandle(&b.arr, c->arr_dev));
+    CUDA_TRY(c, cudaIpcGetMemHandle(&b.rel, c->rel_dev));
+    std::memcpy(out, &b, sizeof b);
+    return DSEA_OK;
+}
+
+dsea_status dsea_ring_connect_peer(dsea_ctx* c, const void* blobs, size_t blob_bytes, int32_t n_blobs)
+{
+    if (!c) return DSEA_EINVAL;
+    if (!c->sliced) return fail(c, DSEA_ESTATE, "dsea_ring_connect_peer before dsea_slice");
+    if (c->NG == 1) return DSEA_OK;
+    if (!blobs || n_blobs != c->NG || blob_bytes != sizeof(PeerBlob))
+        return fail(c, DSEA_EINVAL, "need %d blobs of %zu bytes", c->NG, sizeof(PeerBlob));
+    if (!wait_value32()) return fail(c, DSEA_EPEER, "cuStreamWaitValue32 unavailable");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    const PeerBlob* B = static_cast<const PeerBlob*>(blobs);
+    const int succ = (c->rank + 1) % c->NG, pred = (c->rank - 1 + c->NG) % c->NG;
+    for (int r = 0; r < c->NG; r++)
+        if (B[r].magic != PEER_MAGIC || B[r].rank != r || B[r].ns != c->g.ns)
+            return fail(c, DSEA_EINVAL, "peer blob %d is not a dsea_ring_export of rank %d", r, r);
+    void* p = nullptr;
+    CUDA_TRY(c, cudaIpcOpenMemHandle(&p, B[succ].in, cudaIpcMemLazyEnablePeerAccess));
+    c->succ_in_base = static_cast<char*>(p);
+    CUDA_TRY(c, cudaIpcOpenMemHandle(&p, B[succ].arr, cudaIpcMemLazyEnablePeerAccess));
+    c->succ_arr = static_cast<uint32_t*>(p);
+    CUDA_TRY(c, cudaIpcOpenMemHandle(&p, B[pred].rel, cudaIpcMemLazyEnablePeerAccess));
+    c->pred_rel = static_cast<uint32_t*>(p);
+    c->peer = true;
+    // release counts start at 1 for an initially empty slot, 0 for rank 0's resident state
+    const int ns = c->g.ns;
+    std::vector<uint32_t> init(ns, succ == 0 ? 0u : 1u);
+    CUDA_TRY(c, cudaMemcpy(c->rel_dev, init.data(), sizeof(uint32_t) * ns, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMemset(c->arr_dev, 0, sizeof(uint32_t) * ns));
+    c->wr_cnt.assign(ns, 0u);
+    c->exp_arr.assign(ns, 0u);
+    c->rel_cnt.assign(ns, c->rank == 0 ? 0u : 1u);
+    // the last worker's output buffer is the successor's input buffer (local scratch kept)
+    BufView& last = c->outb[c->W - 1];
+    c->own_outb_last = last.base;
+    last.base = c->succ_in_base;
+    last.remote = 1;
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    c->connected = true;
+    return DSEA_OK;
+}
+
+dsea_status dsea_ring_disconnect(dsea_ctx* c)
+{
+    if (!c) return DSEA_EINVAL;
+    disconnect(c);
+    if (c->connected) {  // NCCL links (destroy is collective: global link order)
+        if (nccl().ok) {
+            const int send_link = c->rank, recv_link = (c->rank - 1 + c->NG) % c->NG;
+            ncclComm_t first = send_link < recv_link ? c->send_comm : c->recv_comm;
+            ncclComm_t second = send_link < recv_link ? c->recv_comm : c->send_comm;
+            if (first) nccl().CommDestroy(first);
+            if (second) nccl().CommDestroy(second);
+        }
+        c->send_comm = c->recv_comm = nullptr;
+        c->connected = false;
+    }
+    return DSEA_OK;
+}
+
 dsea_status dsea_step(dsea_ctx* c, int64_t n_steps)
 {
     if (!c) return DSEA_EINVAL;
@@ -935,6 +1167,7 @@ dsea_status dsea_step(dsea_ctx* c, int64_t n_steps)
     CUDA_TRY(c, cudaStreamSynchronize(c->ss));
     CUDA_TRY(c, cudaStreamSynchronize(c->rs));
     CUDA_TRY(c, cudaStreamSynchronize(c->es));
+    CUDA_TRY(c, cudaStreamSynchronize(c->bs));
     CUDA_TRY(c, cudaGetLastError());
     if ((s = check_dev_err(c))) return s;
 

@@ -62,6 +62,7 @@ struct BufView {
     SlotLayout L;
     int32_t* cnt;    // [ns*ncell] per-cell arrival counters / cursors (not sent)
     int32_t* perm;   // [ns*cap] bin scratch (not sent)
+    int remote;      // slots live in the ring successor's memory (peer backend)
 };
 
 // Device view of a staging buffer (flat SoA over ns*cap entries).
@@ -108,6 +109,7 @@ size_t pipe_smem_bytes(int smax, int maxh);
 int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t* out_cnt,
                  int j0, int nj, UnitEnergy* e_out, double4* partials, unsigned* tickets,
                  DevErr* err, cudaStream_t s);
+void signal_launch(uint32_t* flags, int first, int n, uint32_t value, cudaStream_t s);
 void energy_launch(const Geo& g, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s);
 void bin_scan_launch(const Geo& g, BufView out, int m0, int nm, DevErr* err, cudaStream_t s);
 void bin_place_launch(const Geo& g, BufView out, StgView stg, int s0, int nsrc, int flat_count,

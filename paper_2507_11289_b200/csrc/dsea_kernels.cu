@@ -1016,6 +1016,7 @@ k_bin_scan(Geo g, BufView out, int m0, DevErr* err)
         cs[n] = run;
         if (run > g.cap) set_err(err, DSEA_ECAPACITY, m, -1, run);
     }
+    if (out.remote) __threadfence_system();
 }
 
 // ------------------------------------------------------------------------------
@@ -1101,6 +1102,7 @@ k_bin_gather(Geo g, BufView out, StgView stg, int m0, DevErr* err)
         ofx[d] = stg.fx[src]; ofy[d] = stg.fy[src]; ofz[d] = stg.fz[src];
         oid[d] = id;
     }
+    if (out.remote) __threadfence_system();
 }
 
 // ------------------------------------------------------------------------------
@@ -1218,6 +1220,24 @@ int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t
         k_force<2><<<grid, FORCE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, e_out, partials,
                                                        tickets, err);
     return 1;
+}
+
+// Ring-hop signal (peer backend): after the bin kernels wrote slots [first, first+n)
+// straight into the successor's input buffer over NVLink, publish their arrival
+// count in the successor's flag array (or a release count in the predecessor's).
+__global__ void k_signal(uint32_t* __restrict__ flags, int first, int n, uint32_t value)
+{
+    __threadfence_system();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        volatile uint32_t* f = flags + first + i;
+        *f = value;
+    }
+    __threadfence_system();
+}
+
+void signal_launch(uint32_t* flags, int first, int n, uint32_t value, cudaStream_t s)
+{
+    k_signal<<<1, 64, 0, s>>>(flags, first, n, value);
 }
 
 void energy_launch(const Geo& g, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s)

@@ -81,6 +81,9 @@ SIGNATURES = [
     ("dsea_slice", _st, [_c, ctypes.POINTER(dsea_slice_params)]),
     ("dsea_ring_connect", _st, [_c, ctypes.c_void_p, ctypes.c_int32]),
     ("dsea_ring_unique_id", _st, [ctypes.c_void_p, ctypes.c_size_t]),
+    ("dsea_ring_export", _st, [_c, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    ("dsea_ring_connect_peer", _st, [_c, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32]),
+    ("dsea_ring_disconnect", _st, [_c]),
     ("dsea_step", _st, [_c, ctypes.c_int64]),
     ("dsea_destroy", None, [_c]),
     ("dsea_last_error", ctypes.c_char_p, [_c]),
@@ -160,6 +163,50 @@ def dsea_ring_unique_id() -> bytes:
 def dsea_ring_connect(ctx, ids: bytes, n_ids: int):
     buf = ctypes.create_string_buffer(ids, len(ids))
     _check(ctx, lib.dsea_ring_connect(ctx, buf, n_ids))
+
+
+def dsea_ring_export(ctx) -> bytes:
+    n = ctypes.c_size_t()
+    _check(ctx, lib.dsea_ring_export(ctx, None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value)
+    _check(ctx, lib.dsea_ring_export(ctx, buf, n.value, ctypes.byref(n)))
+    return buf.raw
+
+
+def dsea_ring_connect_peer(ctx, blobs: list):
+    data = b"".join(blobs)
+    buf = ctypes.create_string_buffer(data, len(data))
+    _check(ctx, lib.dsea_ring_connect_peer(ctx, buf, len(blobs[0]), len(blobs)))
+
+
+def ring_connect(ctx, rank: int, world: int, backend: str = "peer"):
+    """Connect one rank of a ring over torch.distributed (plumbing only): "peer" maps
+    the neighbours' slot buffers over NVLink (CUDA IPC); "nccl" opens NCCL p2p links."""
+    import torch.distributed as dist
+    if world == 1:
+        return
+    if backend == "peer":
+        blobs = [None] * world
+        dist.all_gather_object(blobs, dsea_ring_export(ctx))
+        dsea_ring_connect_peer(ctx, blobs)
+    else:
+        ids = [b"".join(dsea_ring_unique_id() for _ in range(world))] if rank == 0 else [None]
+        dist.broadcast_object_list(ids, src=0)
+        dsea_ring_connect(ctx, ids[0], world)
+    dist.barrier()
+
+
+def dsea_ring_disconnect(ctx):
+    _check(ctx, lib.dsea_ring_disconnect(ctx))
+
+
+def ring_disconnect(ctx, world: int):
+    """Collective teardown: close mappings everywhere, barrier, then callers may destroy."""
+    import torch.distributed as dist
+    if world == 1:
+        return
+    dsea_ring_disconnect(ctx)
+    dist.barrier()
 
 
 def dsea_step(ctx, n_steps: int):

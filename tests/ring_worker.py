@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--calls", type=int, default=1)
     ap.add_argument("--block", type=int, default=0, help="slices per stage (0 = auto)")
+    ap.add_argument("--hop", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     rank = int(os.environ["RANK"])
@@ -45,10 +46,7 @@ def main():
     e.slice(n_slices=c.n_slices, cells_per_slice_x=c.cells_per_slice_x, n_gpus=world, rank=rank,
             device=local, workers_per_gpu=a.workers, slices_per_stage=a.block)
     _log(rank, "sliced")
-    ids = [b"".join(D.dsea_ring_unique_id() for _ in range(world))] if rank == 0 else [None]
-    dist.broadcast_object_list(ids, src=0)
-    _log(rank, "ids broadcast")
-    D.dsea_ring_connect(e.ctx, ids[0], world)
+    D.ring_connect(e.ctx, rank, world, a.hop)
     _log(rank, "connected")
     per = a.steps // a.calls
     for k in range(a.calls):
@@ -65,6 +63,7 @@ def main():
                  steps=np.array([s for s, _ in st]), en=np.array([v for _, v in st]),
                  stats=np.array([e.stats().hop_bytes]))
     dist.barrier()
+    D.ring_disconnect(e.ctx, world)
     e.close()
     dist.destroy_process_group()
 

@@ -34,32 +34,34 @@ def _single(cfg, steps):
     return r
 
 
-def _ring(tmp_path, n, cfg, steps, workers=1, calls=1, block=0):
-    out = str(tmp_path / f"ring_{n}_{cfg}_{steps}_{workers}_{calls}_{block}.npz")
+def _ring(tmp_path, n, cfg, steps, workers=1, calls=1, block=0, hop="peer"):
+    out = str(tmp_path / f"ring_{n}_{cfg}_{steps}_{workers}_{calls}_{block}_{hop}.npz")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={29500 + n * 7 + steps}",
            os.path.join(ROOT, "tests", "ring_worker.py"), "--config", cfg, "--steps", str(steps),
-           "--workers", str(workers), "--calls", str(calls), "--block", str(block), "--out", out]
+           "--workers", str(workers), "--calls", str(calls), "--block", str(block), "--hop", hop, "--out", out]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return np.load(out)
 
 
-# (gpus, config, steps, workers, calls, slices per stage; 0 = auto)
-CASES = [(2, "P8", 16, 1, 1, 1), (2, "P8", 9, 1, 2, 1), (2, "P8", 12, 2, 1, 1), (2, "P8", 16, 1, 1, 0),
-         (2, "P8", 10, 2, 2, 3), (4, "P8", 16, 1, 2, 1), (4, "P8", 10, 1, 1, 2), (4, "P8", 16, 1, 1, 0),
-         (8, "P8", 16, 1, 1, 1), (8, "C1", 8, 1, 1, 1), (8, "P8", 24, 1, 2, 0)]
+# (gpus, config, steps, workers, calls, slices per stage (0 = auto), ring hop backend)
+CASES = [(2, "P8", 16, 1, 1, 1, "peer"), (2, "P8", 9, 1, 2, 1, "peer"), (2, "P8", 12, 2, 1, 1, "peer"),
+         (2, "P8", 16, 1, 1, 0, "peer"), (2, "P8", 10, 2, 2, 3, "peer"), (2, "P8", 16, 1, 1, 1, "nccl"),
+         (2, "P8", 10, 2, 2, 3, "nccl"), (4, "P8", 16, 1, 2, 1, "peer"), (4, "P8", 10, 1, 1, 2, "peer"),
+         (4, "P8", 16, 1, 1, 0, "peer"), (4, "P8", 16, 1, 1, 0, "nccl"), (8, "P8", 16, 1, 1, 1, "peer"),
+         (8, "C1", 8, 1, 1, 1, "peer"), (8, "P8", 24, 1, 2, 0, "peer")]
 
 
-@pytest.mark.parametrize("n,cfg,steps,workers,calls,block", CASES)
-def test_ring_bitwise_equals_single_gpu(tmp_path, n, cfg, steps, workers, calls, block):
+@pytest.mark.parametrize("n,cfg,steps,workers,calls,block,hop", CASES)
+def test_ring_bitwise_equals_single_gpu(tmp_path, n, cfg, steps, workers, calls, block, hop):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
     c = CONFIGS[cfg]
     if c.n_slices < 2 + 2 * workers:
         pytest.skip("too few slices")
     x, v, f, s1, e1 = _single(cfg, steps)
-    r = _ring(tmp_path, n, cfg, steps, workers, calls, block)
+    r = _ring(tmp_path, n, cfg, steps, workers, calls, block, hop)
     assert np.array_equal(r["x"], x)
     assert np.array_equal(r["v"], v)
     assert np.array_equal(r["f"], f)
