@@ -829,8 +829,16 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
             int e_np = 0;
             int ho = tid;                        // next free hit-list slot of this lane
             auto flush = [&]() {
-                for (int o = tid; o < ho; o += PIPE_CT) {
-                    const int kk = hl[o];
+                // the two lanes of an atom pool their hit lists and split the combined
+                // list evenly: lane imbalance is then only atom-to-atom variance
+                const int mycnt = (ho - tid) / PIPE_CT;
+                const int other = __shfl_xor_sync(FULLMASK, mycnt, IL);
+                const int c0 = par == 0 ? mycnt : other;           // entries of the par-0 lane
+                const int tot = mycnt + other, half = (tot + 1) >> 1;
+                const int e0 = par == 0 ? 0 : half, e1 = par == 0 ? half : tot;
+                const int t0 = tid & ~IL, t1 = tid | IL;           // hit-list columns of the pair
+                for (int e = e0; e < e1; e++) {
+                    const int kk = e < c0 ? hl[e * PIPE_CT + t0] : hl[(e - c0) * PIPE_CT + t1];
                     const double dx = xi - B.sx[kk];
                     const double dy = yi - B.sy[kk];
                     const double dz = zi - B.sz[kk];
