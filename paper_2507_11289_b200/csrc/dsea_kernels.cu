@@ -565,12 +565,13 @@ size_t pipe_smem_bytes(int smax, int maxh)
     return 2 * per + (size_t)maxh * PIPE_CT * sizeof(uint16_t);
 }
 
+template <int JPAR>
 __global__ void __launch_bounds__(PIPE_THREADS, 2)
 k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt, int j0, int nj,
              DevErr* __restrict__ err, unsigned long long* __restrict__ tile_ctr,
              unsigned long long ctr_base)
 {
-    constexpr int IL = 16;
+    constexpr int IL = 32 / JPAR;           // atoms per chunk; JPAR lanes per atom
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ PipeMeta meta[2];
     __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2];
@@ -769,8 +770,8 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
     const float rc2s = g.rc2_screen;
     const double rc2 = g.rc2;
     const int maxh = T.maxh;
-    constexpr int SEG_PAIRS = 16;           // pairs per lane group per segment
-    constexpr int seg_need = SEG_PAIRS;     // max appends per lane per segment (JPAR = 2)
+    constexpr int SEG_PAIRS = 8 * JPAR;     // candidate pairs per segment (8 per lane)
+    constexpr int seg_need = 16;            // max appends per lane per segment
     const float2 m1 = make_float2(-1.f, -1.f);
     int it = 0;
     for (;;) {
@@ -829,16 +830,24 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
             int e_np = 0;
             int ho = tid;                        // next free hit-list slot of this lane
             auto flush = [&]() {
-                // the two lanes of an atom pool their hit lists and split the combined
+                // the JPAR lanes of an atom pool their hit lists and split the combined
                 // list evenly: lane imbalance is then only atom-to-atom variance
                 const int mycnt = (ho - tid) / PIPE_CT;
-                const int other = __shfl_xor_sync(FULLMASK, mycnt, IL);
-                const int c0 = par == 0 ? mycnt : other;           // entries of the par-0 lane
-                const int tot = mycnt + other, half = (tot + 1) >> 1;
-                const int e0 = par == 0 ? 0 : half, e1 = par == 0 ? half : tot;
-                const int t0 = tid & ~IL, t1 = tid | IL;           // hit-list columns of the pair
+                int pre[JPAR + 1];
+                pre[0] = 0;
+#pragma unroll
+                for (int p = 0; p < JPAR; p++) pre[p + 1] = pre[p] + __shfl_sync(FULLMASK, mycnt, il + p * IL);
+                const int tot = pre[JPAR];
+                const int e0 = (par * tot) / JPAR, e1 = ((par + 1) * tot) / JPAR;
+                const int tcol = tid - lane + il;                  // hit-list column of (il, 0)
                 for (int e = e0; e < e1; e++) {
-                    const int kk = e < c0 ? hl[e * PIPE_CT + t0] : hl[(e - c0) * PIPE_CT + t1];
+                    int p = 0;
+#pragma unroll
+                    for (int u = 1; u < JPAR; u++) p += (e >= pre[u]);
+                    int pb = 0;
+#pragma unroll
+                    for (int u = 1; u < JPAR; u++) pb = (p == u) ? pre[u] : pb;
+                    const int kk = hl[(e - pb) * PIPE_CT + tcol + p * IL];
                     const double dx = xi - B.sx[kk];
                     const double dy = yi - B.sy[kk];
                     const double dz = zi - B.sz[kk];
@@ -877,26 +886,29 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                     const int e = min(phi, s0 + SEG_PAIRS);
                     if (__any_sync(FULLMASK, ho + seg_need * PIPE_CT > maxh * PIPE_CT)) flush();
                     int m = s0 + par;
-                    for (; m + 6 < e; m += 8) {      // 4 pairs: all loads first
-                        const float2 Xa = X2[m], Xb = X2[m + 2], Xc = X2[m + 4], Xd = X2[m + 6];
-                        const float2 Ya = Y2[m], Yb = Y2[m + 2], Yc = Y2[m + 4], Yd = Y2[m + 6];
-                        const float2 Za = Z2[m], Zb = Z2[m + 2], Zc = Z2[m + 4], Zd = Z2[m + 6];
+                    for (; m + 3 * JPAR < e; m += 4 * JPAR) {      // 4 pairs: all loads first
+                        const float2 Xa = X2[m], Xb = X2[m + JPAR], Xc = X2[m + 2 * JPAR], Xd = X2[m + 3 * JPAR];
+                        const float2 Ya = Y2[m], Yb = Y2[m + JPAR], Yc = Y2[m + 2 * JPAR], Yd = Y2[m + 3 * JPAR];
+                        const float2 Za = Z2[m], Zb = Z2[m + JPAR], Zc = Z2[m + 2 * JPAR], Zd = Z2[m + 3 * JPAR];
                         screen(Xa, Ya, Za, 2 * m);
-                        screen(Xb, Yb, Zb, 2 * m + 4);
-                        screen(Xc, Yc, Zc, 2 * m + 8);
-                        screen(Xd, Yd, Zd, 2 * m + 12);
+                        screen(Xb, Yb, Zb, 2 * (m + JPAR));
+                        screen(Xc, Yc, Zc, 2 * (m + 2 * JPAR));
+                        screen(Xd, Yd, Zd, 2 * (m + 3 * JPAR));
                     }
-                    for (; m < e; m += 2) screen(X2[m], Y2[m], Z2[m], 2 * m);
+                    for (; m < e; m += JPAR) screen(X2[m], Y2[m], Z2[m], 2 * m);
                 }
             }
             flush();
             // combine the two parity lanes of each atom (fixed order)
-            fx += __shfl_xor_sync(FULLMASK, fx, IL);
-            fy += __shfl_xor_sync(FULLMASK, fy, IL);
-            fz += __shfl_xor_sync(FULLMASK, fz, IL);
-            e_u += __shfl_xor_sync(FULLMASK, e_u, IL);
-            e_v += __shfl_xor_sync(FULLMASK, e_v, IL);
-            e_np += __shfl_xor_sync(FULLMASK, e_np, IL);
+#pragma unroll
+            for (int o = IL; o < 32; o <<= 1) {   // fixed xor tree over the atom's lanes
+                fx += __shfl_xor_sync(FULLMASK, fx, o);
+                fy += __shfl_xor_sync(FULLMASK, fy, o);
+                fz += __shfl_xor_sync(FULLMASK, fz, o);
+                e_u += __shfl_xor_sync(FULLMASK, e_u, o);
+                e_v += __shfl_xor_sync(FULLMASK, e_v, o);
+                e_np += __shfl_xor_sync(FULLMASK, e_np, o);
+            }
             if (valid && par == 0) {
                 const double Fx = 24.0 * fx, Fy = 24.0 * fy, Fz = 24.0 * fz;
                 double vx = vx0, vy = vy0, vz = vz0;
@@ -1146,7 +1158,8 @@ static size_t force_smem_bytes(int smax, int jpar, int maxh)
 }
 
 
-static size_t pipe_smem_attr = 0;    // largest dynamic smem set on k_force_pipe so far
+static size_t pipe_smem_attr = 0;    // largest dynamic smem set on k_force_pipe<2> so far
+static size_t pipe_smem_attr4 = 0;   // ... on k_force_pipe<4>
 
 static double env_num(const char* name, double dflt)
 {
@@ -1178,6 +1191,7 @@ Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
     T.tiles = g.c * g.cells[1] * T.nzt;
     T.pipe = env_num("DSEA_FORCE_V2", 0) == 0;
     if (T.pipe) {
+        T.jpar = (int)env_num("DSEA_PIPE_JPAR", 2) == 4 ? 4 : 2;
         T.smax = ((int)(env_num("DSEA_PIPE_MARGIN", 1.2) * expected + 64.0) + 31) / 32 * 32;
         while (T.smax > 32 && pipe_smem_bytes(T.smax, T.maxh) > (size_t)smem_optin) T.smax -= 32;
         if (T.smax > 65504) T.smax = 65504;
@@ -1190,16 +1204,16 @@ int force_kernel_attr(const Tiling& T)
 {
     if (T.pipe) {
         // the attribute is process-wide: keep the largest request of any context
-        if (T.smem > pipe_smem_attr) {
-            cudaError_t e = cudaFuncSetAttribute(k_force_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)T.smem);
+        auto kern = T.jpar == 4 ? k_force_pipe<4> : k_force_pipe<2>;
+        size_t& attr = T.jpar == 4 ? pipe_smem_attr4 : pipe_smem_attr;
+        if (T.smem > attr) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem);
             if (e != cudaSuccess) return -1;
-            pipe_smem_attr = T.smem;
+            attr = T.smem;
         }
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force_pipe, PIPE_THREADS, T.smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PIPE_THREADS, T.smem);
         if (per_sm < 1) return -1;
-
         return per_sm;
     }
     cudaError_t e = T.jpar == 4
@@ -1215,8 +1229,12 @@ int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t
     if (T.pipe) {
         // the tile counter is never reset: each launch consumes exactly ntiles + grid
         // increments, so the host tracks the base of every launch
-        k_force_pipe<<<T.grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err,
-                                                          T.ctr, *T.ctr_base);
+        if (T.jpar == 4)
+            k_force_pipe<4><<<T.grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err,
+                                                                 T.ctr, *T.ctr_base);
+        else
+            k_force_pipe<2><<<T.grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err,
+                                                                 T.ctr, *T.ctr_base);
         *T.ctr_base += (unsigned long long)nj * T.tiles + T.grid;
         return 1;
     }
