@@ -1063,40 +1063,41 @@ k_bin_place(Geo g, BufView out, StgView stg, int s0, int flat_count, int m0, int
 }
 
 // ------------------------------------------------------------------------------
-// Bin pass 3: one warp per cell sorts its arrivals by (z, id) -- a data-determined
-// order, identical for every schedule -- and gathers them from staging into the
-// slot; resets the cell's counter for the next fill.
+// Bin pass 3: one half-warp per cell (cells hold ~13 atoms at rho 0.8) sorts its
+// arrivals by (z, id) -- a data-determined order, identical for every schedule --
+// and gathers them from staging into the slot; resets the cell's counter.
 // ------------------------------------------------------------------------------
 constexpr int GATHER_THREADS = 256;
-constexpr int GATHER_WARPS = GATHER_THREADS / 32;
-constexpr int CELL_MAX = 256;
+constexpr int GATHER_CELLS = GATHER_THREADS / 16;   // cells per CTA
+constexpr int CELL_MAX = 128;
 
 __global__ void __launch_bounds__(GATHER_THREADS)
 k_bin_gather(Geo g, BufView out, StgView stg, int m0, DevErr* err)
 {
-    __shared__ double kz[GATHER_WARPS][CELL_MAX];
-    __shared__ int kid[GATHER_WARPS][CELL_MAX];
-    __shared__ int ksrc[GATHER_WARPS][CELL_MAX];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ double kz[GATHER_CELLS][CELL_MAX];
+    __shared__ int kid[GATHER_CELLS][CELL_MAX];
+    __shared__ int ksrc[GATHER_CELLS][CELL_MAX];
+    const int sub = threadIdx.x & 15, hw = threadIdx.x >> 4;
+    const unsigned hmask = 0xffffu << (threadIdx.x & 16);
     const int m = m0 + blockIdx.y;
-    const int c = blockIdx.x * GATHER_WARPS + warp;
+    const int c = blockIdx.x * GATHER_CELLS + hw;
     if (c >= g.ncell) return;
     const int32_t* cs = slot_cs(out, m);
     const int st = cs[c], en = cs[c + 1];
-    if (lane == 0) out.cnt[(size_t)m * g.ncell + c] = 0;
+    if (sub == 0) out.cnt[(size_t)m * g.ncell + c] = 0;
     if (cs[g.ncell] > g.cap) return;  // capacity error already flagged by the scan
     const int n = en - st;
     if (n > CELL_MAX) {
-        if (lane == 0) set_err(err, DSEA_ECAPACITY, m, -1, n);
+        if (sub == 0) set_err(err, DSEA_ECAPACITY, m, -1, n);
         return;
     }
-    for (int e = lane; e < n; e += 32) {
+    for (int e = sub; e < n; e += 16) {
         const int src = out.perm[(size_t)m * g.cap + st + e];
-        ksrc[warp][e] = src;
-        kz[warp][e] = stg.z[src];
-        kid[warp][e] = stg.id[src];
+        ksrc[hw][e] = src;
+        kz[hw][e] = stg.z[src];
+        kid[hw][e] = stg.id[src];
     }
-    __syncwarp();
+    __syncwarp(hmask);
     double* ox = slot_d(out, m, out.L.off_x);
     double* oy = slot_d(out, m, out.L.off_y);
     double* oz = slot_d(out, m, out.L.off_z);
@@ -1107,15 +1108,15 @@ k_bin_gather(Geo g, BufView out, StgView stg, int m0, DevErr* err)
     double* ofy = slot_d(out, m, out.L.off_fy);
     double* ofz = slot_d(out, m, out.L.off_fz);
     int32_t* oid = slot_i(out, m, out.L.off_id);
-    for (int e = lane; e < n; e += 32) {
-        const double z = kz[warp][e];
-        const int id = kid[warp][e];
+    for (int e = sub; e < n; e += 16) {
+        const double z = kz[hw][e];
+        const int id = kid[hw][e];
         int rank = 0;
         for (int e2 = 0; e2 < n; e2++) {
-            const double z2 = kz[warp][e2];
-            rank += (z2 < z) || (z2 == z && kid[warp][e2] < id);
+            const double z2 = kz[hw][e2];
+            rank += (z2 < z) || (z2 == z && kid[hw][e2] < id);
         }
-        const int src = ksrc[warp][e];
+        const int src = ksrc[hw][e];
         const int d = st + rank;
         ox[d] = stg.x[src]; oy[d] = stg.y[src]; oz[d] = z;
         ovx[d] = stg.vx[src]; ovy[d] = stg.vy[src]; ovz[d] = stg.vz[src];
@@ -1292,7 +1293,7 @@ void bin_place_launch(const Geo& g, BufView out, StgView stg, int s0, int nsrc, 
 void bin_gather_launch(const Geo& g, BufView out, StgView stg, int m0, int nm, DevErr* err,
                        cudaStream_t s)
 {
-    dim3 grid((g.ncell + GATHER_WARPS - 1) / GATHER_WARPS, nm);
+    dim3 grid((g.ncell + GATHER_CELLS - 1) / GATHER_CELLS, nm);
     k_bin_gather<<<grid, GATHER_THREADS, 0, s>>>(g, out, stg, m0, err);
 }
 
