@@ -211,6 +211,8 @@ struct dsea_ctx {
     unsigned* tickets = nullptr;
     DevErr* err_dev = nullptr;
     unsigned long long* tile_ctr = nullptr;
+    double* aos_dev = nullptr;            // [3 * 3N] by-id AoS scratch for set_state / get_*
+    unsigned long long* count_dev = nullptr;
     unsigned long long tile_ctr_base = 0;
     std::vector<cudaEvent_t> ev_recv, ev_free, ev_bin, ev_send;
     std::vector<cudaEvent_t> ev_force, ev_energy;   // per worker: force done / energies done
@@ -498,25 +500,30 @@ dsea_status check_dev_err(dsea_ctx* c)
 }
 
 // Bin the flat host state (by id) into the slots of the input buffer.
+dsea_status ensure_aos(dsea_ctx* c)
+{
+    if (c->aos_dev) return DSEA_OK;
+    dsea_status s;
+    if ((s = dalloc(c, &c->aos_dev, (size_t)9 * c->N))) return s;
+    if ((s = dalloc(c, &c->count_dev, 1))) return s;
+    return DSEA_OK;
+}
+
 dsea_status upload_state(dsea_ctx* c, const double* xyz, const double* v, const double* f)
 {
+    // contiguous copies of the caller's by-id arrays; the AoS -> SoA split runs on the GPU
     const int64_t N = c->N;
-    std::vector<double> soa((size_t)N * 9);
-    std::vector<int32_t> ids((size_t)N);
-    for (int64_t i = 0; i < N; i++) {
-        for (int d = 0; d < 3; d++) {
-            soa[(size_t)d * N + i] = xyz[3 * i + d];
-            soa[(size_t)(3 + d) * N + i] = v[3 * i + d];
-            soa[(size_t)(6 + d) * N + i] = f ? f[3 * i + d] : 0.0;
-        }
-        ids[(size_t)i] = (int32_t)i;
-    }
+    dsea_status s;
+    if ((s = ensure_aos(c))) return s;
+    double* dx = c->aos_dev;
+    double* dv = c->aos_dev + 3 * (size_t)N;
+    double* df = c->aos_dev + 6 * (size_t)N;
+    CUDA_TRY(c, cudaMemcpyAsync(dx, xyz, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, c->cs));
+    CUDA_TRY(c, cudaMemcpyAsync(dv, v, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, c->cs));
+    if (f) CUDA_TRY(c, cudaMemcpyAsync(df, f, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, c->cs));
     StgView& S = c->stg[0];
-    double* dst[] = {S.x, S.y, S.z, S.vx, S.vy, S.vz, S.fx, S.fy, S.fz};
-    for (int a = 0; a < 9; a++)
-        CUDA_TRY(c, cudaMemcpyAsync(dst[a], soa.data() + (size_t)a * N, sizeof(double) * N,
-                                    cudaMemcpyHostToDevice, c->cs));
-    CUDA_TRY(c, cudaMemcpyAsync(S.id, ids.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, c->cs));
+    aos_to_stage_launch(S, dx, dv, f ? df : nullptr, (int)N, c->cs);
+    c->stats.kernel_launches++;
     init_keys_launch(c->g, S, (int)N, c->inb.cnt, c->err_dev, c->cs);
     bin_scan_launch(c->g, c->inb, 0, c->g.ns, c->err_dev, c->cs);
     bin_place_launch(c->g, c->inb, S, 0, 0, (int)N, 0, c->g.ns, c->err_dev, c->cs);
@@ -524,8 +531,7 @@ dsea_status upload_state(dsea_ctx* c, const double* xyz, const double* v, const 
     c->stats.kernel_launches += 4;
     CUDA_TRY(c, cudaStreamSynchronize(c->cs));
     CUDA_TRY(c, cudaGetLastError());
-    dsea_status s = check_dev_err(c);
-    if (s) return s;
+    if ((s = check_dev_err(c))) return s;
     c->holds_state = true;
     c->mirror_valid = false;
     return DSEA_OK;
@@ -565,18 +571,18 @@ dsea_status get_vec(dsea_ctx* c, double* out, int64_t n, int which)
         return DSEA_OK;
     }
     if (!c->holds_state) return fail(c, DSEA_ESTATE, "this rank does not hold the state (rank 0 does)");
-    dsea_status s = fetch_mirror(c);
+    // scatter by id on the GPU, then one contiguous device-to-host copy
+    dsea_status s = ensure_aos(c);
     if (s) return s;
-    const size_t off[3][3] = {{c->L.off_x, c->L.off_y, c->L.off_z},
-                              {c->L.off_vx, c->L.off_vy, c->L.off_vz},
-                              {c->L.off_fx, c->L.off_fy, c->L.off_fz}};
-    int64_t seen = 0;
-    for_each_atom(c, [&](int, int i, int, int id, const char* base) {
-        for (int d = 0; d < 3; d++)
-            out[3 * (int64_t)id + d] = reinterpret_cast<const double*>(base + off[which][d])[i];
-        seen++;
-    });
-    if (seen != c->N) return fail(c, DSEA_ESTATE, "slots hold %lld atoms, expected %lld", (long long)seen, (long long)c->N);
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemsetAsync(c->count_dev, 0, sizeof(unsigned long long), c->cs));
+    slots_to_aos_launch(c->g, c->inb, which, c->aos_dev, c->count_dev, c->cs);
+    unsigned long long seen = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(out, c->aos_dev, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->cs));
+    CUDA_TRY(c, cudaMemcpyAsync(&seen, c->count_dev, sizeof seen, cudaMemcpyDeviceToHost, c->cs));
+    CUDA_TRY(c, cudaStreamSynchronize(c->cs));
+    if ((int64_t)seen != c->N)
+        return fail(c, DSEA_ESTATE, "slots hold %llu atoms, expected %lld", seen, (long long)c->N);
     return DSEA_OK;
 }
 

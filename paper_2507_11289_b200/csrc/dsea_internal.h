@@ -109,6 +109,9 @@ size_t pipe_smem_bytes(int smax, int maxh);
 int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t* out_cnt,
                  int j0, int nj, UnitEnergy* e_out, double4* partials, unsigned* tickets,
                  DevErr* err, cudaStream_t s);
+void aos_to_stage_launch(StgView S, const double* xyz, const double* v, const double* f, int n, cudaStream_t s);
+void slots_to_aos_launch(const Geo& g, BufView in, int which, double* out, unsigned long long* count,
+                         cudaStream_t s);
 void signal_launch(uint32_t* flags, int first, int n, uint32_t value, cudaStream_t s);
 void energy_launch(const Geo& g, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s);
 void bin_scan_launch(const Geo& g, BufView out, int m0, int nm, DevErr* err, cudaStream_t s);

@@ -1149,6 +1149,55 @@ __global__ void k_init_keys(Geo g, StgView stg, int n, int32_t* __restrict__ out
 }
 
 // ------------------------------------------------------------------------------
+// Host-facing conversions done on the device: by-id AoS arrays (the ABI layout) to
+// staging SoA on upload, and slot SoA back to by-id AoS on read-back, so that the
+// host only issues contiguous copies.
+// ------------------------------------------------------------------------------
+__global__ void k_aos_to_stage(StgView S, const double* __restrict__ xyz, const double* __restrict__ v,
+                               const double* __restrict__ f, int n)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    S.x[p] = xyz[3 * (size_t)p]; S.y[p] = xyz[3 * (size_t)p + 1]; S.z[p] = xyz[3 * (size_t)p + 2];
+    S.vx[p] = v[3 * (size_t)p]; S.vy[p] = v[3 * (size_t)p + 1]; S.vz[p] = v[3 * (size_t)p + 2];
+    if (f) { S.fx[p] = f[3 * (size_t)p]; S.fy[p] = f[3 * (size_t)p + 1]; S.fz[p] = f[3 * (size_t)p + 2]; }
+    else { S.fx[p] = 0.0; S.fy[p] = 0.0; S.fz[p] = 0.0; }
+    S.id[p] = p;
+}
+
+__global__ void k_slots_to_aos(Geo g, BufView in, int which, double* __restrict__ out,
+                               unsigned long long* __restrict__ count)
+{
+    const int j = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = slot_cs(in, j)[g.ncell];
+    const bool ok = i < n;
+    if (ok) {
+        const size_t o0 = which == 0 ? in.L.off_x : which == 1 ? in.L.off_vx : in.L.off_fx;
+        const size_t o1 = which == 0 ? in.L.off_y : which == 1 ? in.L.off_vy : in.L.off_fy;
+        const size_t o2 = which == 0 ? in.L.off_z : which == 1 ? in.L.off_vz : in.L.off_fz;
+        const size_t id = (size_t)slot_i(in, j, in.L.off_id)[i];
+        out[3 * id] = slot_d(in, j, o0)[i];
+        out[3 * id + 1] = slot_d(in, j, o1)[i];
+        out[3 * id + 2] = slot_d(in, j, o2)[i];
+    }
+    const unsigned b = __ballot_sync(FULLMASK, ok);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, (unsigned long long)__popc(b));
+}
+
+void aos_to_stage_launch(StgView S, const double* xyz, const double* v, const double* f, int n, cudaStream_t s)
+{
+    k_aos_to_stage<<<(n + 255) / 256, 256, 0, s>>>(S, xyz, v, f, n);
+}
+
+void slots_to_aos_launch(const Geo& g, BufView in, int which, double* out, unsigned long long* count,
+                         cudaStream_t s)
+{
+    dim3 grid((g.cap + 255) / 256, g.ns);
+    k_slots_to_aos<<<grid, 256, 0, s>>>(g, in, which, out, count);
+}
+
+// ------------------------------------------------------------------------------
 // Host-side launchers
 // ------------------------------------------------------------------------------
 static size_t force_smem_bytes(int smax, int jpar, int maxh)
