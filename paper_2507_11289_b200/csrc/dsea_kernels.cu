@@ -660,7 +660,7 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                         const int grp = lane - lane % 3;
                         const int coltot = __shfl_sync(FULLMASK, cnt, grp) + __shfl_sync(FULLMASK, cnt, min(grp + 1, 31)) +
                                            __shfl_sync(FULLMASK, cnt, min(grp + 2, 31));
-                        const int span = cnt + ((lane < 27 && lane % 3 == 2) ? ((4 - (coltot & 3)) & 3) : 0);
+                        const int span = cnt + ((lane < 27 && lane % 3 == 2) ? (coltot & 1) : 0);
                         int incl = span;
 #pragma unroll
                         for (int o = 1; o < 32; o <<= 1) {
@@ -701,9 +701,9 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                         const int lo = pt_dst[3 * lane], hi = pt_end[3 * lane + 2];
                         M.c_lo[lane] = lo;
                         M.c_hi[lane] = hi;
-                        for (int d = hi; d < lo + ((hi - lo + 3) & ~3); d++) {  // far-away dummies
-                            B.fx[d] = 1e30f; B.fy[d] = 1e30f; B.fz[d] = 1e30f;
-                            B.sx[d] = 1e300; B.sy[d] = 1e300; B.sz[d] = 1e300;
+                        if ((hi - lo) & 1) {  // far-away dummy: never passes the screen
+                            B.fx[hi] = 1e30f; B.fy[hi] = 1e30f; B.fz[hi] = 1e30f;
+                            B.sx[hi] = 1e300; B.sy[hi] = 1e300; B.sz[hi] = 1e300;
                         }
                     }
                     if (lane == 0) {
@@ -767,7 +767,7 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
     const float rc2s = g.rc2_screen;
     const double rc2 = g.rc2;
     const int maxh = T.maxh;
-    constexpr int SEG_QUADS = 4 * JPAR;     // candidate quads per segment (4 per lane)
+    constexpr int SEG_PAIRS = 8 * JPAR;     // candidate pairs per segment (8 per lane)
     constexpr int seg_need = 16;            // max appends per lane per segment
     const float2 m1 = make_float2(-1.f, -1.f);
     int it = 0;
@@ -779,9 +779,9 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
         const PipeBuf B = pipe_buf(smem, T.smax, b);
         const int j = M.j, nhome = M.nhome, self_base = M.self_base, home_first = M.home_first;
         const int nchunks = M.nchunks;
-        const float4* X4 = reinterpret_cast<const float4*>(B.fx);
-        const float4* Y4 = reinterpret_cast<const float4*>(B.fy);
-        const float4* Z4 = reinterpret_cast<const float4*>(B.fz);
+        const float2* X2 = reinterpret_cast<const float2*>(B.fx);
+        const float2* Y2 = reinterpret_cast<const float2*>(B.fy);
+        const float2* Z2 = reinterpret_cast<const float2*>(B.fz);
         for (;;) {
             int chv = 0;
             if (lane == 0) chv = atomicAdd(&M.next_chunk, 1);
@@ -803,11 +803,11 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                 if (lane < 9) {
                     const double key = zmin - g.rc - 1e-9;
                     while (lo < hi) { const int mid = (lo + hi) >> 1; if (B.sz[mid] < key) lo = mid + 1; else hi = mid; }
-                    wb = base + ((lo - base) & ~3);            // down to a quad start
+                    wb = base + ((lo - base) & ~1);
                 } else {
                     const double key = zmax + g.rc + 1e-9;
                     while (lo < hi) { const int mid = (lo + hi) >> 1; if (B.sz[mid] <= key) lo = mid + 1; else hi = mid; }
-                    wb = base + ((lo - base + 3) & ~3);        // up to a quad end (dummies)
+                    wb = base + ((lo - base + 1) & ~1);
                 }
             }
             // integration inputs of this lane's atom, loaded now, used after the pair work
@@ -875,26 +875,24 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                 if (r2.x <= rc2s) { hl[ho] = (uint16_t)k; ho += PIPE_CT; }
                 if (r2.y <= rc2s) { hl[ho] = (uint16_t)(k + 1); ho += PIPE_CT; }
             };
-            auto screen4 = [&](const float4 X, const float4 Y, const float4 Z, const int k) {
-                screen(make_float2(X.x, X.y), make_float2(Y.x, Y.y), make_float2(Z.x, Z.y), k);
-                screen(make_float2(X.z, X.w), make_float2(Y.z, Y.w), make_float2(Z.z, Z.w), k + 2);
-            };
 #pragma unroll 1
             for (int col = 0; col < 9; col++) {
-                const int qlo = __shfl_sync(FULLMASK, wb, col) >> 2;
-                const int qhi = __shfl_sync(FULLMASK, wb, 16 + col) >> 2;
-                for (int s0 = qlo; s0 < qhi; s0 += SEG_QUADS) {
-                    const int e = min(qhi, s0 + SEG_QUADS);
+                const int plo = __shfl_sync(FULLMASK, wb, col) >> 1;
+                const int phi = __shfl_sync(FULLMASK, wb, 16 + col) >> 1;
+                for (int s0 = plo; s0 < phi; s0 += SEG_PAIRS) {
+                    const int e = min(phi, s0 + SEG_PAIRS);
                     if (__any_sync(FULLMASK, ho + seg_need * PIPE_CT > maxh * PIPE_CT)) flush();
-                    int q = s0 + par;
-                    for (; q + JPAR < e; q += 2 * JPAR) {      // 2 quads: all loads first
-                        const float4 Xa = X4[q], Xb = X4[q + JPAR];
-                        const float4 Ya = Y4[q], Yb = Y4[q + JPAR];
-                        const float4 Za = Z4[q], Zb = Z4[q + JPAR];
-                        screen4(Xa, Ya, Za, 4 * q);
-                        screen4(Xb, Yb, Zb, 4 * (q + JPAR));
+                    int m = s0 + par;
+                    for (; m + 3 * JPAR < e; m += 4 * JPAR) {      // 4 pairs: all loads first
+                        const float2 Xa = X2[m], Xb = X2[m + JPAR], Xc = X2[m + 2 * JPAR], Xd = X2[m + 3 * JPAR];
+                        const float2 Ya = Y2[m], Yb = Y2[m + JPAR], Yc = Y2[m + 2 * JPAR], Yd = Y2[m + 3 * JPAR];
+                        const float2 Za = Z2[m], Zb = Z2[m + JPAR], Zc = Z2[m + 2 * JPAR], Zd = Z2[m + 3 * JPAR];
+                        screen(Xa, Ya, Za, 2 * m);
+                        screen(Xb, Yb, Zb, 2 * (m + JPAR));
+                        screen(Xc, Yc, Zc, 2 * (m + 2 * JPAR));
+                        screen(Xd, Yd, Zd, 2 * (m + 3 * JPAR));
                     }
-                    for (; q < e; q += JPAR) screen4(X4[q], Y4[q], Z4[q], 4 * q);
+                    for (; m < e; m += JPAR) screen(X2[m], Y2[m], Z2[m], 2 * m);
                 }
             }
             flush();
