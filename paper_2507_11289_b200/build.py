@@ -61,6 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if force or _stale(o, [s] + hdrs):
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xptxas", "-v", "-fmad=true",
+                  *os.environ.get("DSEA_NVCC_EXTRA", "").split(),   # -D sweeps (use --force)
                   "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o], verbose)
         objs.append(o)
     for src in SOURCES_CPP:

@@ -494,10 +494,17 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
 // Energies are written per atom (u, v, ke, pairs) and reduced per slice in a fixed
 // order by k_energy, so the result does not depend on which warp took which chunk.
 // ------------------------------------------------------------------------------
-constexpr int PIPE_CWARPS = 4;                      // consumer warps
+#ifndef DSEA_PIPE_CW
+#define DSEA_PIPE_CW 4
+#endif
+#ifndef DSEA_PIPE_HOME
+#define DSEA_PIPE_HOME (DSEA_PIPE_CW * 16)
+#endif
+constexpr int PIPE_CWARPS = DSEA_PIPE_CW;           // consumer warps
 constexpr int PIPE_CT = 32 * PIPE_CWARPS;           // consumer threads (hit-list columns)
 constexpr int PIPE_THREADS = PIPE_CT + 64;          // + two producer warps
-constexpr int PIPE_HOME = PIPE_CWARPS * 16;         // home atoms per tile
+constexpr int PIPE_MINB = PIPE_CWARPS >= 8 ? 1 : 2; // resident CTAs per SM
+constexpr int PIPE_HOME = DSEA_PIPE_HOME;           // home atoms per tile
 constexpr int PIPE_PAD = 64;                        // slack after each staged array
 
 struct PipeMeta {
@@ -563,7 +570,7 @@ size_t pipe_smem_bytes(int smax, int maxh)
 }
 
 template <int JPAR>
-__global__ void __launch_bounds__(PIPE_THREADS, 2)
+__global__ void __launch_bounds__(PIPE_THREADS, PIPE_MINB)
 k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt, int j0, int nj,
              DevErr* __restrict__ err, unsigned long long* __restrict__ tile_ctr,
              unsigned long long ctr_base)
@@ -828,7 +835,12 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
             int ho = tid;                        // next free hit-list slot of this lane
             auto flush = [&]() {
                 // the JPAR lanes of an atom pool their hit lists and split the combined
-                // list evenly: lane imbalance is then only atom-to-atom variance
+                // list evenly: lane imbalance is then only atom-to-atom variance.
+                // Lanes read each other's lists: warp barriers order those reads after
+                // the owners' appends and before the owners append the next segment
+                // (without the second one a lane leaving the divergent loop early can
+                // overwrite entries its partner has not read yet).
+                __syncwarp();
                 const int mycnt = (ho - tid) / PIPE_CT;
                 int pre[JPAR + 1];
                 pre[0] = 0;
@@ -863,6 +875,7 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                         e_np += 1;
                     }
                 }
+                __syncwarp();
                 ho = tid;
             };
             auto screen = [&](const float2 X, const float2 Y, const float2 Z, const int k) {
@@ -881,7 +894,9 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                 const int phi = __shfl_sync(FULLMASK, wb, 16 + col) >> 1;
                 for (int s0 = plo; s0 < phi; s0 += SEG_PAIRS) {
                     const int e = min(phi, s0 + SEG_PAIRS);
-                    if (__any_sync(FULLMASK, ho + seg_need * PIPE_CT > maxh * PIPE_CT)) flush();
+                    // flush on the entry count only: the decision must not depend on which
+                    // warp (tid) took the chunk, or the summation order would
+                    if (__any_sync(FULLMASK, ho - tid + seg_need * PIPE_CT > maxh * PIPE_CT)) flush();
                     int m = s0 + par;
                     for (; m + 3 * JPAR < e; m += 4 * JPAR) {      // 4 pairs: all loads first
                         const float2 Xa = X2[m], Xb = X2[m + JPAR], Xc = X2[m + 2 * JPAR], Xd = X2[m + 3 * JPAR];
@@ -1239,7 +1254,12 @@ Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
     T.pipe = env_num("DSEA_FORCE_V2", 0) == 0;
     if (T.pipe) {
         T.jpar = (int)env_num("DSEA_PIPE_JPAR", 2) == 4 ? 4 : 2;
-        T.smax = ((int)(env_num("DSEA_PIPE_MARGIN", 1.2) * expected + 64.0) + 31) / 32 * 32;
+        T.nzt = std::max(1, (int)std::ceil(1.25 * mean_col / PIPE_HOME) + 1);
+        T.tiles = g.c * g.cells[1] * T.nzt;
+        const double per_col_p = std::min(mean_col + 2.0 * mean_per_cell,
+                                          PIPE_HOME + (2.0 * g.rc + g.l[2]) * dens);
+        const double expected_p = 9.0 * per_col_p + 18.0;
+        T.smax = ((int)(env_num("DSEA_PIPE_MARGIN", 1.2) * expected_p + 64.0) + 31) / 32 * 32;
         while (T.smax > 32 && pipe_smem_bytes(T.smax, T.maxh) > (size_t)smem_optin) T.smax -= 32;
         if (T.smax > 65504) T.smax = 65504;
         T.smem = pipe_smem_bytes(T.smax, T.maxh);

@@ -171,6 +171,30 @@ def test_ring_of_one_bitwise_equals_fused(W, B):
     assert np.array_equal(e1, e2)
 
 
+@pytest.mark.parametrize("maxh,rc", [("24", 2.5), ("40", 2.5), ("", 4.0)])
+def test_deterministic_with_mid_chunk_flushes(monkeypatch, maxh, rc):
+    """Hit lists shorter than one chunk's hits (small DSEA_MAXH, or rc = 4.0 with ~107
+    hits per lane) force flushes in the middle of a chunk; the result must still not
+    depend on which warp or CTA took the chunk: reruns and the staged path are
+    bitwise equal to the fused path."""
+    from paper_2507_11289_b200.configs import Config
+    if maxh:
+        monkeypatch.setenv("DSEA_MAXH", maxh)
+    c = Config("d", 30 if rc > 3 else 20, 8, 8, 0, rc=rc)
+
+    def run(**kw):
+        e, _ = _engine(c, **kw)
+        e.step(4)
+        r = e.positions(), e.velocities(), e.forces(), e.energies()[1]
+        e.close()
+        return r
+    a, b = run(), run()
+    s = run(workers_per_gpu=2, mode=D.DSEA_MODE_STAGED, slices_per_stage=1)
+    for x, y, z in zip(a, b, s):
+        assert np.array_equal(x, y)
+        assert np.array_equal(x, z)
+
+
 def test_deterministic_rerun():
     a, _ = _engine("C1")
     b, _ = _engine("C1")
