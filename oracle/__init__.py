@@ -59,12 +59,15 @@ def lib():
         L.oracle_normal.restype = _d
         L.oracle_velocities.argtypes = [_i64, _u64, _d, _pd]
         L.oracle_velocities.restype = None
-        L.oracle_forces.argtypes = [_i64, _pd, _pd, _d, _pd, _pd, _pd, _pd, _i]
+        L.oracle_forces.argtypes = [_i64, _pd, _pd, _d, _pd, _pd, _pd, _pd, _pd, _i]
         L.oracle_forces.restype = None
         L.oracle_forces_subset.argtypes = [_i64, _pd, _pd, _d, _i64, _pi64, _pd, _pd, _i]
         L.oracle_forces_subset.restype = None
         L.oracle_run.argtypes = [_i64, _pd, _pd, _pd, _pd, _d, _d, _i64, _pd, _i]
+        L.oracle_run_ex.argtypes = [_i64, _pd, _pd, _pd, _pd, _d, _d, _i64, _pd, _i, _d, _pd, _pi32,
+                                    _i, _i, _pd]
         L.oracle_run.restype = _i
+        L.oracle_run_ex.restype = _i
         L.oracle_bin.argtypes = [_i64, _pd, _pd, _pi32, _i, _pi32, _pi32]
         L.oracle_bin.restype = None
         L.oracle_nmax.argtypes = [_i, _i, _i, _i]
@@ -135,10 +138,12 @@ def forces(xyz, box, rc, nthreads=None, per_atom=False):
     U = ctypes.c_double()
     V = ctypes.c_double()
     Ui = np.zeros(n) if per_atom else None
+    Vi = np.zeros(n) if per_atom else None
     lib().oracle_forces(n, _p(xyz), _p(box), rc, _p(F), ctypes.byref(U), ctypes.byref(V),
-                        _p(Ui) if per_atom else None, nthreads or default_threads())
+                        _p(Ui) if per_atom else None, _p(Vi) if per_atom else None,
+                        nthreads or default_threads())
     if per_atom:
-        return F, U.value, V.value, Ui
+        return F, U.value, V.value, Ui, Vi
     return F, U.value, V.value
 
 
@@ -165,6 +170,40 @@ def run(xyz, v, F, box, rc, dt, nsteps, nthreads=None):
     if rv != 0:
         raise MemoryError("oracle_run failed")
     return xyz, v, F, e
+
+
+def run_ex(xyz, v, F, box, rc, dt, nsteps, geom, T_target=None, nthreads=None):
+    """Algorithm 1 with the optional per-slice NVT thermostat (reading Q23)
+    and per-slice records.  geom: oracle.geometry(...) of the same box.  Returns
+    (xyz, v, F, energies[nsteps, 4], slice_rec[nsteps, n_slices, 4] = {n, U, V, KE})."""
+    xyz = np.array(xyz, dtype=np.float64, order="C")
+    v = np.array(v, dtype=np.float64, order="C")
+    F = np.array(F, dtype=np.float64, order="C")
+    box = np.ascontiguousarray(box, dtype=np.float64)
+    l = np.ascontiguousarray(geom.l, dtype=np.float64)
+    cells = np.ascontiguousarray(geom.cells, dtype=np.int32)
+    ns = int(geom.n_slices)
+    e = np.zeros((max(nsteps, 0), 4))
+    rec = np.zeros((max(nsteps, 0), ns, 4))
+    rv = lib().oracle_run_ex(xyz.shape[0], _p(xyz), _p(v), _p(F), _p(box), rc, dt, nsteps, _p(e),
+                             nthreads or default_threads(), -1.0 if T_target is None else float(T_target),
+                             _p(l), _p(cells, _pi32), int(geom.cells[0]) // ns, ns, _p(rec))
+    if rv != 0:
+        raise RuntimeError(f"oracle_run_ex failed ({rv})")
+    return xyz, v, F, e, rec
+
+
+def pressure(KE, V, n_atoms, volume):
+    """Virial pressure from Algorithm 1's accumulators ("virial V (for pressure
+    calculation)"): p = rho T + W / (3 Vol) with T = 2 KE / (3 N) and the virial
+    W = sum_{i<j} r_ij . F_ij = 24 V (Alg. 1 accumulates (2 r^-12 - r^-6) / 2 per
+    ordered pair, i.e. W / 24).  Works elementwise on arrays (x-resolved profiles:
+    per-slice KE, V, n and the slice volume)."""
+    KE = np.asarray(KE, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    n = np.asarray(n_atoms, dtype=np.float64)
+    T = np.divide(2.0 * KE, 3.0 * n, out=np.zeros_like(KE * n), where=n > 0)
+    return (n / volume) * T + 24.0 * V / (3.0 * volume)
 
 
 def bin_atoms(xyz, l, cells, c=1):

@@ -24,7 +24,9 @@
  * F = -grad U by finite differences; LJ minimum at 2^(1/6); cutoff inclusivity
  * and shifted-energy continuity; virial identity sum r.F = 24 V; Newton's third
  * law; explicit periodic-image brute force; FCC shell sums; NVE drift and its
- * dt^2 scaling; time reversibility through wall hits.  Parity unpinned: the
+ * dt^2 scaling; time reversibility through wall hits; NVT: every slice at
+ * T_target after the scaling, long-run mean temperature, per-slice records summing
+ * to the totals, configurational pressure = -dU/dVol by finite differences.  Parity unpinned: the
  * paper prints no per-atom values, so the exact mirror rule (Q2) and the
  * velocity generator (Q9) are pinned by our own contract, not by the paper.
  */
@@ -172,7 +174,7 @@ static void pair_sum_for_atom(int64_t i, int64_t n, const double *xyz, double by
 }
 
 void oracle_forces(int64_t n, const double *xyz, const double *box, double rc,
-                   double *F, double *U, double *V, double *Ui, int nthreads)
+                   double *F, double *U, double *V, double *Ui, double *Vi, int nthreads)
 {
     double by = box[1], bz = box[2];
     double rc2 = rc * rc;
@@ -190,6 +192,7 @@ void oracle_forces(int64_t n, const double *xyz, const double *box, double rc,
     double su = 0.0, sv = 0.0;
     for (int64_t i = 0; i < n; i++) { su += ui[i]; sv += vi[i]; }
     if (Ui) memcpy(Ui, ui, sizeof(double) * (size_t)n);
+    if (Vi) memcpy(Vi, vi, sizeof(double) * (size_t)n);
     *U = su; *V = sv;
     free(ui); free(vi);
 }
@@ -219,6 +222,9 @@ void oracle_forces_subset(int64_t n, const double *xyz, const double *box, doubl
 /*    negate v_x and the stored F_new,x.                                */
 /* y, z: periodic wrap into [0, b) (Q1).                                */
 /* ------------------------------------------------------------------ */
+void oracle_bin(int64_t n, const double *xyz, const double *l, const int32_t *cells, int c,
+                int32_t *cell_xyz, int32_t *slice);
+
 static void apply_boundaries(double *r, double *v, double *f, const double *box)
 {
     if (r[0] < 0.0) {
@@ -237,17 +243,41 @@ static void apply_boundaries(double *r, double *v, double *f, const double *box)
 /* (F_new = 0 at entry on a fresh state).  State arrays are [3N] by id; */
 /* F holds F_new on entry and on exit.  energies: [nsteps][4] =         */
 /* {U, KE, V, E=U+KE} with E_n = U(r_n) + KE(v_n) (Q12).                 */
+/*                                                                      */
+/* Optional NVT thermostat (T_target > 0), §4.1: after the    */
+/* kick (md_v3aa) the scale factor is computed per slice (md_thermo_a/b)*/
+/* and applied before the position update (md_v3b).  Reading Q23:       */
+/* isokinetic, lambda_j = sqrt(T_target / T_j) with T_j = sum v.v /     */
+/* (3 n_j) over the atoms of slice j (membership = binning of r at the  */
+/* start of the step); lambda_j = 1 for an empty or motionless slice.   */
+/* KE in energies stays the post-kick, pre-scale value.                 */
+/* slice_rec (optional): [nsteps][n_slices][4] = {n_j, U_j, V_j, KE_j}, */
+/* U_j, V_j = sums of the per-atom Algorithm-1 shares of the slice's    */
+/* atoms, KE_j = post-kick, pre-scale kinetic energy of the slice.      */
 /* ------------------------------------------------------------------ */
-int oracle_run(int64_t n, double *xyz, double *v, double *F, const double *box, double rc,
-               double dt, int64_t nsteps, double *energies, int nthreads)
+int oracle_run_ex(int64_t n, double *xyz, double *v, double *F, const double *box, double rc,
+                  double dt, int64_t nsteps, double *energies, int nthreads, double T_target,
+                  const double *l, const int32_t *cells, int c, int n_slices, double *slice_rec)
 {
-    double *Fold = (double *)malloc(sizeof(double) * (size_t)(3 * n > 0 ? 3 * n : 1));
-    if (!Fold) return -1;
+    const int need_slices = (T_target > 0.0) || slice_rec;
+    size_t n1 = (size_t)(n > 0 ? n : 1);
+    double *Fold = (double *)malloc(sizeof(double) * 3 * n1);
+    double *ui = (double *)malloc(sizeof(double) * n1);
+    double *vi = (double *)malloc(sizeof(double) * n1);
+    int32_t *cxyz = (int32_t *)malloc(sizeof(int32_t) * 3 * n1);
+    int32_t *sl = (int32_t *)malloc(sizeof(int32_t) * n1);
+    double *ke_j = (double *)malloc(sizeof(double) * (size_t)(n_slices > 0 ? n_slices : 1));
+    double *cnt_j = (double *)malloc(sizeof(double) * (size_t)(n_slices > 0 ? n_slices : 1));
+    int rv = 0;
+    if (!Fold || !ui || !vi || !cxyz || !sl || !ke_j || !cnt_j) { rv = -1; goto done; }
+    if (need_slices && (!l || !cells || c < 1 || n_slices < 1)) { rv = -2; goto done; }
     for (int64_t step = 0; step < nsteps; step++) {
+        /* slice membership of every atom at the start of the step */
+        if (need_slices) oracle_bin(n, xyz, l, cells, c, cxyz, sl);
         /* F_old = F_new ; F_new = sum over neighbours */
         memcpy(Fold, F, sizeof(double) * (size_t)(3 * n));
         double U, V;
-        oracle_forces(n, xyz, box, rc, F, &U, &V, NULL, nthreads);
+        oracle_forces(n, xyz, box, rc, F, &U, &V, ui, vi, nthreads);
         /* v = v + (F_new + F_old) * 0.5 * dt */
         for (int64_t i = 0; i < 3 * n; i++) v[i] = v[i] + (F[i] + Fold[i]) * 0.5 * dt;
         double ke = 0.0;
@@ -260,12 +290,52 @@ int oracle_run(int64_t n, double *xyz, double *v, double *F, const double *box, 
             energies[4 * step + 2] = V;
             energies[4 * step + 3] = U + ke;
         }
+        if (need_slices) {
+            for (int j = 0; j < n_slices; j++) { ke_j[j] = 0.0; cnt_j[j] = 0.0; }
+            for (int64_t i = 0; i < n; i++) {
+                const double vv = v[3 * i] * v[3 * i] + v[3 * i + 1] * v[3 * i + 1] + v[3 * i + 2] * v[3 * i + 2];
+                ke_j[sl[i]] += vv;
+                cnt_j[sl[i]] += 1.0;
+            }
+            if (slice_rec) {
+                double *rec = slice_rec + (size_t)step * n_slices * 4;
+                for (int j = 0; j < n_slices; j++) {
+                    rec[4 * j + 0] = cnt_j[j];
+                    rec[4 * j + 1] = 0.0;
+                    rec[4 * j + 2] = 0.0;
+                    rec[4 * j + 3] = 0.5 * ke_j[j];
+                }
+                for (int64_t i = 0; i < n; i++) {
+                    rec[4 * sl[i] + 1] += ui[i];
+                    rec[4 * sl[i] + 2] += vi[i];
+                }
+            }
+            if (T_target > 0.0) {
+                /* md_thermo_a/b + the scaling in md_v3b, reading Q23 */
+                for (int j = 0; j < n_slices; j++) {
+                    const double Tj = (cnt_j[j] > 0.0) ? ke_j[j] / (3.0 * cnt_j[j]) : 0.0;
+                    ke_j[j] = (Tj > 0.0) ? sqrt(T_target / Tj) : 1.0;   /* lambda_j */
+                }
+                for (int64_t i = 0; i < n; i++) {
+                    const double lam = ke_j[sl[i]];
+                    v[3 * i] *= lam; v[3 * i + 1] *= lam; v[3 * i + 2] *= lam;
+                }
+            }
+        }
         /* r = r + v*dt + F_new*0.5*dt^2 */
         for (int64_t i = 0; i < 3 * n; i++) xyz[i] = xyz[i] + v[i] * dt + F[i] * 0.5 * (dt * dt);
         for (int64_t i = 0; i < n; i++) apply_boundaries(&xyz[3 * i], &v[3 * i], &F[3 * i], box);
     }
-    free(Fold);
-    return 0;
+done:
+    free(Fold); free(ui); free(vi); free(cxyz); free(sl); free(ke_j); free(cnt_j);
+    return rv;
+}
+
+int oracle_run(int64_t n, double *xyz, double *v, double *F, const double *box, double rc,
+               double dt, int64_t nsteps, double *energies, int nthreads)
+{
+    return oracle_run_ex(n, xyz, v, F, box, rc, dt, nsteps, energies, nthreads, -1.0, NULL, NULL,
+                         1, 0, NULL);
 }
 
 /* ------------------------------------------------------------------ */

@@ -188,7 +188,7 @@ def test_minimum_image_equals_explicit_image_sum():
             tiles.append(xyz + np.array([0.0, (ny + 1) * box[1], (nz + 1) * box[2]]))
     big = np.concatenate(tiles)
     big_box = np.array([box[0], 3 * box[1], 3 * box[2]])
-    Fb, _, _, Ub = oracle.forces(big, big_box, RC, per_atom=True)
+    Fb, _, _, Ub, _ = oracle.forces(big, big_box, RC, per_atom=True)
     n = len(xyz)
     assert np.allclose(Fb[:n], F, rtol=1e-12, atol=1e-12)
     assert abs(Ub[:n].sum() - U) < 1e-11 * abs(U)
@@ -204,7 +204,7 @@ def test_fcc_shell_sums():
         nx = 12 if rc < 3 else 14
         g = oracle.geometry(nx, 8 if rc < 3 else 9, 8 if rc < 3 else 9, rho, rc, 1, 1)
         x = oracle.lattice(nx, 8 if rc < 3 else 9, 8 if rc < 3 else 9, g.a)
-        F, _, _, Ui = oracle.forces(x, g.b, rc, per_atom=True)
+        F, _, _, Ui, _ = oracle.forces(x, g.b, rc, per_atom=True)
         center = np.argmin(np.abs(x[:, 0] - g.b[0] / 2) + np.abs(x[:, 1] - g.b[1] / 2) + np.abs(x[:, 2] - g.b[2] / 2))
         assert x[center, 0] > rc + 1 and x[center, 0] < g.b[0] - rc - 1
         us = (1 / rc) ** 6 - (1 / rc) ** 12
@@ -327,3 +327,83 @@ def test_eq1_nmax():
     assert oracle.nmax(10, 1, 0, 0) == 5
     assert oracle.nmax(64, 2) == 10
     assert oracle.nmax(109, 1) == 27
+
+
+# --------------------------------------------------------------------------- NVT (NEXT-1)
+def _nvt_state(seed=3, T0=1.0):
+    """N = 500 (5^3 FCC cells) at rho = 0.5, the SPEC's thermostat system,
+    jittered, with Gaussian velocities at T0."""
+    g = oracle.geometry(5, 5, 5, 0.5, RC)
+    x = inputs.jitter(oracle.lattice(5, 5, 5, g.a), g.b, 0.2, seed)
+    v = inputs.gaussian_velocities(len(x), T0, seed)
+    return g, x, v
+
+
+def test_nvt_every_slice_at_target_after_scaling():
+    """P:314-316 (md_thermo_a/b compute the scale factor; md_v3b scales), reading Q23:
+    after one step every slice's kinetic temperature sum v.v / (3 n_j) -- recomputed
+    here from the returned velocities, grouped by the binning of the INPUT positions --
+    equals T_target.  Catches lambda without the sqrt, a KE factor slip, global instead
+    of per-slice scaling, or membership taken after the drift."""
+    g, x, v = _nvt_state()
+    _, sl = oracle.bin_atoms(x, g.l, g.cells, 1)
+    assert len(np.unique(sl)) == g.n_slices
+    _, v1, _, e, rec = oracle.run_ex(x, v, np.zeros_like(x), g.b, RC, 0.0018, 1, g, T_target=1.5)
+    for j in range(g.n_slices):
+        m = sl == j
+        Tj = (v1[m] ** 2).sum() / (3 * m.sum())
+        assert abs(Tj - 1.5) < 1e-12, (j, Tj)
+    # the recorded KE is the post-kick, pre-scale value: not at T_target
+    assert abs(2 * e[0, 1] / (3 * len(x)) - 1.5) > 0.05
+
+
+def test_nvt_off_equals_nve_and_slice_records_sum_to_totals():
+    """run_ex without a thermostat is Algorithm 1 exactly (bitwise equal to run), and
+    the per-slice records {n, U, V, KE} sum to the domain totals every step (x-resolved
+    results, P:325)."""
+    g, x, v = _nvt_state(seed=4)
+    a = oracle.run(x, v, np.zeros_like(x), g.b, RC, 0.0018, 5)
+    b = oracle.run_ex(x, v, np.zeros_like(x), g.b, RC, 0.0018, 5, g)
+    for p, q in zip(a, b[:4]):
+        assert np.array_equal(p, q)
+    rec, e = b[4], b[3]
+    assert np.all(rec[:, :, 0].sum(1) == len(x))
+    assert np.allclose(rec[:, :, 1].sum(1), e[:, 0], rtol=1e-12)
+    assert np.allclose(rec[:, :, 2].sum(1), e[:, 2], rtol=1e-12)
+    assert np.allclose(rec[:, :, 3].sum(1), e[:, 1], rtol=1e-12)
+
+
+def test_nvt_long_run_mean_temperature():
+    """SPEC S:322 / S:492 anchored on P:322 ("temperature of k_B T / eps = 1.5"): from
+    the rho = 0.5 lattice with velocities at T0 = 1.0, the time-averaged kinetic
+    temperature over steps 500-1500 is within 1 % of T_target = 1.5, while the NVE run
+    from the same start is not (so the thermostat, not the start, sets it)."""
+    g = oracle.geometry(5, 5, 5, 0.5, RC)
+    x = oracle.lattice(5, 5, 5, g.a)
+    v = oracle.velocities(len(x), 7, 1.0)
+    *_, e_nvt, _ = oracle.run_ex(x, v, np.zeros_like(x), g.b, RC, 0.0018, 1500, g, T_target=1.5)
+    T = 2 * e_nvt[500:, 1] / (3 * len(x))
+    assert abs(T.mean() / 1.5 - 1) < 0.01, T.mean()
+    _, _, _, e_nve = oracle.run(x, v, np.zeros_like(x), g.b, RC, 0.0018, 1500)
+    T0 = 2 * e_nve[500:, 1] / (3 * len(x))
+    assert abs(T0.mean() / 1.5 - 1) > 0.05
+
+
+def test_configurational_pressure_is_minus_dU_dVol():
+    """Pressure from Algorithm 1's virial accumulator: for a static
+    configuration p = -dU/dVol under homogeneous scaling of positions and box (y/z
+    periodic, x walls: U depends only on pair distances), by central differences of
+    the oracle's U alone.  Pins oracle.pressure's 24 V / (3 Vol) (a wrong factor 8 vs
+    24, or V vs 2V, fails by >= 2x)."""
+    box = np.array([9.0, 8.0, 7.7])
+    x = inputs.random_points(60, box, seed=12, min_sep=0.95)
+    _, U, V = oracle.forces(x, box, RC)
+    vol = box.prod()
+    h = 1e-6
+    up = oracle.forces(x * (1 + h), box * (1 + h), RC)[1]
+    um = oracle.forces(x * (1 - h), box * (1 - h), RC)[1]
+    p_fd = -((up - um) / (2 * h)) / (3 * vol)
+    p = oracle.pressure(0.0, V, len(x), vol)
+    assert abs(p - p_fd) < 1e-6 * max(1.0, abs(p_fd)), (p, p_fd)
+    # ideal-gas limit: no pair within rc -> p = rho T
+    assert abs(oracle.pressure(3.0, 0.0, 10, 5.0) - (10 / 5.0) * (2 * 3.0 / 30)) < 1e-15
