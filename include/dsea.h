@@ -112,6 +112,20 @@ typedef struct {
     double V;          /* virial accumulator of Alg. 1 */
 } dsea_energy;
 
+/* x-resolved observables of one slice (§4.2 "DSEAmd yields spatially
+ * resolved results"; reading Q24), summed over the timesteps this rank computed
+ * since the last dsea_reset_profiles.  Per timestep the slice contributes its atom
+ * count, the sums of its atoms' Algorithm 1 shares of U and V and its
+ * post-kick kinetic energy.  Time averages are sum / samples; the slice volume is
+ * w * b_y * b_z, so p_j = (n_j T_j + 8 V_j) / Vol_j with T_j = 2 KE_j / (3 n_j). */
+typedef struct {
+    int64_t samples;   /* timesteps accumulated */
+    double n_sum;      /* sum of the slice's atom count */
+    double U_sum;      /* sum of the slice's potential energy */
+    double V_sum;      /* sum of the slice's virial accumulator */
+    double KE_sum;     /* sum of the slice's kinetic energy (after the kick, before scaling) */
+} dsea_profile;
+
 /* Counters for the benchmark harness (filled by dsea_get_stats). */
 typedef struct {
     int64_t kernel_launches;   /* kernels this context launched since the last reset */
@@ -207,6 +221,22 @@ dsea_status dsea_get_energies(dsea_ctx *ctx, dsea_energy *out, int64_t cap, int6
  * x [0,b_z).  On a multi-GPU ring only rank 0 stores it (other ranks: no-op). */
 dsea_status dsea_set_state(dsea_ctx *ctx, const double *xyz, const double *vxyz,
                            const double *fxyz_or_null, int64_t n_atoms);
+
+/* NVT thermostat (§4.1: md_thermo_a/b compute the velocity scale factor,
+ * md_v3b applies it; reading Q23).  enable != 0: every slice, every timestep, after
+ * the kick: lambda_j = sqrt(T_target / T_j), T_j = sum v.v / (3 n_j) over the slice's
+ * atoms (lambda = 1 for an empty or motionless slice), v <- lambda_j v, then the
+ * position update.  Per slice, so the ring needs no extra exchange.  Energies keep
+ * the post-kick (pre-scale) KE.  DSEA_EINVAL if enable and T_target <= 0 or not
+ * finite; DSEA_ESTATE before dsea_slice or with the non-default DSEA_FORCE_V2 kernel.
+ * Applies from the next dsea_step; on a ring every rank must set the same value. */
+dsea_status dsea_set_thermostat(dsea_ctx *ctx, int32_t enable, double T_target);
+
+/* Per-slice sums (dsea_profile) for slices 0..n_slices-1; n_slices must equal N_S
+ * (DSEA_EINVAL otherwise).  On a ring each rank holds the timesteps it computed;
+ * the caller sums over ranks.  dsea_reset_profiles zeroes them (dsea_slice does). */
+dsea_status dsea_get_profiles(dsea_ctx *ctx, dsea_profile *out, int32_t n_slices);
+dsea_status dsea_reset_profiles(dsea_ctx *ctx);
 
 /* ---- instrumentation ---------------------------------------------------------- */
 

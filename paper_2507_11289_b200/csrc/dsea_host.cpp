@@ -239,6 +239,7 @@ struct dsea_ctx {
     bool holds_state = false;
 
     std::vector<dsea_energy> energies;
+    std::vector<dsea_profile> prof;       // per slice, x-resolved sums (Q24)
     int64_t steps_done = 0;
 
     bool timing = false;
@@ -660,7 +661,13 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                              c->e_dev + (size_t)op.t_rel * ns, c->partials, c->tickets, c->err_dev, c->cs);
             c->stats.force_launches++;
             if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_FORCE, {t0, t1}}); }
-            if (c->T.pipe) {  // per-slice energy reduction off the critical path
+            if (c->T.pipe && c->g.thermo) {  // NVT: lambda_j on the critical path, then the drift
+                UnitEnergy* eo = c->e_dev + (size_t)op.t_rel * ns;
+                energy_launch(c->g, c->stg[w], j, n, eo, c->cs);
+                drift_launch(c->g, c->stg[w], j, n, eo, c->outb[w].cnt, c->err_dev, c->cs);
+                CUDA_TRY(c, cudaEventRecord(c->ev_energy[w], c->cs));
+                c->stats.kernel_launches += 2;
+            } else if (c->T.pipe) {  // per-slice energy reduction off the critical path
                 CUDA_TRY(c, cudaEventRecord(c->ev_force[w], c->cs));
                 CUDA_TRY(c, cudaStreamWaitEvent(c->es, c->ev_force[w], 0));
                 energy_launch(c->g, c->stg[w], j, n, c->e_dev + (size_t)op.t_rel * ns, c->es);
@@ -818,7 +825,13 @@ dsea_status run_fused(dsea_ctx* c, int64_t n_steps)
         if (c->T.pipe) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_energy[0], 0));
         int nl = force_launch(c->g, c->T, c->inb, c->stg[0], c->inb.cnt, 0, ns,
                               c->e_dev + (size_t)t * ns, c->partials, c->tickets, c->err_dev, c->cs);
-        if (c->T.pipe) {
+        if (c->T.pipe && c->g.thermo) {  // NVT: lambda_j, then the drift
+            UnitEnergy* eo = c->e_dev + (size_t)t * ns;
+            energy_launch(c->g, c->stg[0], 0, ns, eo, c->cs);
+            drift_launch(c->g, c->stg[0], 0, ns, eo, c->inb.cnt, c->err_dev, c->cs);
+            CUDA_TRY(c, cudaEventRecord(c->ev_energy[0], c->cs));
+            nl += 2;
+        } else if (c->T.pipe) {
             CUDA_TRY(c, cudaEventRecord(c->ev_force[0], c->cs));
             CUDA_TRY(c, cudaStreamWaitEvent(c->es, c->ev_force[0], 0));
             energy_launch(c->g, c->stg[0], 0, ns, c->e_dev + (size_t)t * ns, c->es);
@@ -961,6 +974,8 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     g.ncell = g.c * geo.cells[1] * geo.cells[2];
     g.cap = geo.slot_capacity;
     g.rc2_screen = (float)(g.rc2 * (1.0 + 1e-5) + 1e-3);
+    g.thermo = 0;          // NVE until dsea_set_thermostat
+    g.T_target = 0.0;
     c->L = make_slot_layout(g.ncell, g.cap);
 
     int optin = 0;
@@ -980,6 +995,7 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->bs, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_cs, cudaEventDisableTiming));
     c->sliced = true;
+    c->prof.assign((size_t)c->g.ns, dsea_profile{});
 
     // buffers: input buffer + one output buffer per worker; the last worker of a ring
     // of one writes straight back into the input buffer (local hand-off).
@@ -1198,6 +1214,12 @@ dsea_status dsea_step(dsea_ctx* c, int64_t n_steps)
         for (int j = 0; j < ns; j++) {
             const UnitEnergy& e = he[(size_t)t * ns + j];
             uc += e.u_core; v2 += e.vir2; k2 += e.ke2; np += e.npairs;
+            dsea_profile& pr = c->prof[j];
+            pr.samples += 1;
+            pr.n_sum += e.natoms;
+            pr.U_sum += 2.0 * e.u_core + 2.0 * c->g.ushift * e.npairs;
+            pr.V_sum += 0.5 * e.vir2;
+            pr.KE_sum += 0.5 * e.ke2;
         }
         dsea_energy r;
         r.step = c->steps_done + t;
@@ -1255,6 +1277,34 @@ dsea_status dsea_get_cells(dsea_ctx* c, int32_t* cell_xyz, int32_t* slice, int64
         cell_xyz[3 * (int64_t)id + 2] = cell % CZ;
         slice[id] = j;
     });
+    return DSEA_OK;
+}
+
+dsea_status dsea_set_thermostat(dsea_ctx* c, int32_t enable, double T_target)
+{
+    if (!c) return DSEA_EINVAL;
+    if (enable && !(std::isfinite(T_target) && T_target > 0.0))
+        return fail(c, DSEA_EINVAL, "thermostat temperature must be > 0 (got %g)", T_target);
+    if (!c->sliced) return fail(c, DSEA_ESTATE, "dsea_set_thermostat before dsea_slice");
+    if (enable && !c->T.pipe) return fail(c, DSEA_ESTATE, "the thermostat needs the default force kernel");
+    c->g.thermo = enable ? 1 : 0;
+    c->g.T_target = enable ? T_target : 0.0;
+    return DSEA_OK;
+}
+
+dsea_status dsea_get_profiles(dsea_ctx* c, dsea_profile* out, int32_t n_slices)
+{
+    if (!c || !out) return DSEA_EINVAL;
+    if (!c->sliced) return fail(c, DSEA_ESTATE, "dsea_get_profiles before dsea_slice");
+    if (n_slices != c->g.ns) return fail(c, DSEA_EINVAL, "%d slices expected", c->g.ns);
+    for (int j = 0; j < n_slices; j++) out[j] = c->prof[(size_t)j];
+    return DSEA_OK;
+}
+
+dsea_status dsea_reset_profiles(dsea_ctx* c)
+{
+    if (!c) return DSEA_EINVAL;
+    for (auto& p : c->prof) p = dsea_profile{};
     return DSEA_OK;
 }
 

@@ -30,6 +30,8 @@ struct Geo {
     int ncell;      // cells per slice = c * cells[1] * cells[2]
     int cap;        // atoms per slot
     float rc2_screen;  // fp32 pre-screen radius^2 (rc^2 + margin)
+    int thermo;        // NVT: per-slice isokinetic scaling before the drift (Q23)
+    double T_target;   // thermostat temperature
 };
 
 struct SlotLayout {
@@ -94,6 +96,8 @@ struct UnitEnergy {
     double vir2;     // sum of s6*(2 s6 - 1)  (V = vir2 / 2)
     double ke2;      // sum of v.v after the kick (KE = ke2 / 2)
     double npairs;   // number of in-cutoff ordered pairs
+    double natoms;   // atoms of the slice at this timestep
+    double lambda;   // thermostat scale factor of the slice (1 without thermostat)
 };
 
 // Error record written by kernels (first error wins).
@@ -114,6 +118,10 @@ void slots_to_aos_launch(const Geo& g, BufView in, int which, double* out, unsig
                          cudaStream_t s);
 void signal_launch(uint32_t* flags, int first, int n, uint32_t value, cudaStream_t s);
 void energy_launch(const Geo& g, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s);
+// NVT only: v <- lambda_j v, then the drift/walls/destination of md_v3b for the
+// staged atoms of slices [j0, j0+nj) (lambda_j from e_out[j], written by k_energy)
+void drift_launch(const Geo& g, StgView stg, int j0, int nj, const UnitEnergy* e_out, int32_t* out_cnt,
+                  DevErr* err, cudaStream_t s);
 void bin_scan_launch(const Geo& g, BufView out, int m0, int nm, DevErr* err, cudaStream_t s);
 void bin_place_launch(const Geo& g, BufView out, StgView stg, int s0, int nsrc, int flat_count,
                       int m0, int nm, DevErr* err, cudaStream_t s);

@@ -494,6 +494,42 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
 // Energies are written per atom (u, v, ke, pairs) and reduced per slice in a fixed
 // order by k_energy, so the result does not depend on which warp took which chunk.
 // ------------------------------------------------------------------------------
+// Position update of md_v3b for one atom whose kick is done:
+// drift, mirror in x (Q2), wrap in y/z (Q1), destination slot/cell (must be j-1, j
+// or j+1, else EUNSTABLE), staging stores and the arrival count of the cell.
+__device__ __forceinline__ void drift_store(const Geo& g, const StgView& stg, size_t st, int j, double xi,
+                                            double yi, double zi, double vx, double vy, double vz, double Fx,
+                                            double Fy, double Fz, int id, int32_t* __restrict__ out_cnt,
+                                            DevErr* __restrict__ err)
+{
+    const int CY = g.cells[1], CZ = g.cells[2];
+    const double hdt2 = 0.5 * (g.dt * g.dt);
+    double x = xi + vx * g.dt + Fx * hdt2;
+    double y = yi + vy * g.dt + Fy * hdt2;
+    double z = zi + vz * g.dt + Fz * hdt2;
+    double Fxn = Fx;
+    if (x < 0.0) { x = -x; vx = -vx; Fxn = -Fxn; }                       // Q2
+    else if (x > g.b[0]) { x = 2.0 * g.b[0] - x; vx = -vx; Fxn = -Fxn; }
+    if (y < 0.0) y += g.b[1]; else if (y >= g.b[1]) y -= g.b[1];         // Q1
+    if (z < 0.0) z += g.b[2]; else if (z >= g.b[2]) z -= g.b[2];
+    const int cxg = cell_coord(x, g.l[0], g.cells[0]);
+    const int cyg = cell_coord(y, g.l[1], CY);
+    const int czg = cell_coord(z, g.l[2], CZ);
+    const int m = cxg / g.c;
+    if (!(isfinite(x) && isfinite(y) && isfinite(z)) || m < j - 1 || m > j + 1) {
+        set_err(err, DSEA_EUNSTABLE, j, id, m);
+        stg.key[st] = -1;
+    } else {
+        const int key = m * g.ncell + ((cxg - m * g.c) * CY + cyg) * CZ + czg;
+        stg.x[st] = x; stg.y[st] = y; stg.z[st] = z;
+        stg.vx[st] = vx; stg.vy[st] = vy; stg.vz[st] = vz;
+        stg.fx[st] = Fxn; stg.fy[st] = Fy; stg.fz[st] = Fz;
+        stg.id[st] = id;
+        stg.key[st] = key;
+        atomicAdd(&out_cnt[key], 1);
+    }
+}
+
 #ifndef DSEA_PIPE_CW
 #define DSEA_PIPE_CW 4
 #endif
@@ -923,39 +959,22 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
             }
             if (valid && par == 0) {
                 const double Fx = 24.0 * fx, Fy = 24.0 * fy, Fz = 24.0 * fz;
-                double vx = vx0, vy = vy0, vz = vz0;
-                const int id = aid;
                 const double hdt = 0.5 * g.dt;
-                vx = vx + (Fx + fxo) * hdt;
-                vy = vy + (Fy + fyo) * hdt;
-                vz = vz + (Fz + fzo) * hdt;
+                const double vx = vx0 + (Fx + fxo) * hdt;
+                const double vy = vy0 + (Fy + fyo) * hdt;
+                const double vz = vz0 + (Fz + fzo) * hdt;
                 const double ke2 = vx * vx + vy * vy + vz * vz;
-                const double hdt2 = 0.5 * (g.dt * g.dt);
-                double x = xi + vx * g.dt + Fx * hdt2;
-                double y = yi + vy * g.dt + Fy * hdt2;
-                double z = zi + vz * g.dt + Fz * hdt2;
-                double Fxn = Fx;
-                if (x < 0.0) { x = -x; vx = -vx; Fxn = -Fxn; }                       // Q2
-                else if (x > g.b[0]) { x = 2.0 * g.b[0] - x; vx = -vx; Fxn = -Fxn; }
-                if (y < 0.0) y += g.b[1]; else if (y >= g.b[1]) y -= g.b[1];         // Q1
-                if (z < 0.0) z += g.b[2]; else if (z >= g.b[2]) z -= g.b[2];
-                const int cxg = cell_coord(x, g.l[0], g.cells[0]);
-                const int cyg = cell_coord(y, g.l[1], CY);
-                const int czg = cell_coord(z, g.l[2], CZ);
-                const int m = cxg / g.c;
                 const size_t st = (size_t)j * g.cap + gi;
                 stg.eatom[st] = make_double4(e_u, e_v, ke2, (double)e_np);
-                if (!(isfinite(x) && isfinite(y) && isfinite(z)) || m < j - 1 || m > j + 1) {
-                    set_err(err, DSEA_EUNSTABLE, j, id, m);
-                    stg.key[st] = -1;
-                } else {
-                    const int key = m * g.ncell + ((cxg - m * g.c) * CY + cyg) * CZ + czg;
-                    stg.x[st] = x; stg.y[st] = y; stg.z[st] = z;
+                if (g.thermo) {
+                    // NVT: the slice's scale factor needs every atom's kick first
+                    // (k_energy -> lambda_j, then k_drift finishes md_v3b)
+                    stg.x[st] = xi; stg.y[st] = yi; stg.z[st] = zi;
                     stg.vx[st] = vx; stg.vy[st] = vy; stg.vz[st] = vz;
-                    stg.fx[st] = Fxn; stg.fy[st] = Fy; stg.fz[st] = Fz;
-                    stg.id[st] = id;
-                    stg.key[st] = key;
-                    atomicAdd(&out_cnt[key], 1);
+                    stg.fx[st] = Fx; stg.fy[st] = Fy; stg.fz[st] = Fz;
+                    stg.id[st] = aid;
+                } else {
+                    drift_store(g, stg, st, j, xi, yi, zi, vx, vy, vz, Fx, Fy, Fz, aid, out_cnt, err);
                 }
             }
         }
@@ -995,7 +1014,31 @@ k_energy(Geo g, StgView stg, int j0, UnitEnergy* __restrict__ e_out)
         for (int w = 0; w < ENERGY_THREADS / 32; w++) { A += s[w][0]; B += s[w][1]; C += s[w][2]; D += s[w][3]; }
         UnitEnergy ue;
         ue.u_core = A; ue.vir2 = B; ue.ke2 = C; ue.npairs = D;
+        ue.natoms = (double)n;
+        // md_thermo_a/b, reading Q23: lambda_j = sqrt(T_target / T_j),
+        // T_j = sum v.v / (3 n_j) after the kick; 1 for an empty or motionless slice
+        double lam = 1.0;
+        if (g.thermo && n > 0 && C > 0.0) lam = sqrt(g.T_target / (C / (3.0 * (double)n)));
+        ue.lambda = lam;
         e_out[j] = ue;
+    }
+}
+
+// NVT: scale the kicked velocities of slice j by lambda_j (the velocity scaling of
+// md_v3b), then the position update and destination as in the NVE path.
+constexpr int DRIFT_THREADS = 256;
+
+__global__ void __launch_bounds__(DRIFT_THREADS)
+k_drift(Geo g, StgView stg, int j0, const UnitEnergy* __restrict__ e_out, int32_t* __restrict__ out_cnt,
+        DevErr* __restrict__ err)
+{
+    const int j = j0 + blockIdx.y;
+    const int n = stg.n[j];
+    const double lam = e_out[j].lambda;
+    for (int i = blockIdx.x * DRIFT_THREADS + threadIdx.x; i < n; i += gridDim.x * DRIFT_THREADS) {
+        const size_t st = (size_t)j * g.cap + i;
+        drift_store(g, stg, st, j, stg.x[st], stg.y[st], stg.z[st], lam * stg.vx[st], lam * stg.vy[st],
+                    lam * stg.vz[st], stg.fx[st], stg.fy[st], stg.fz[st], stg.id[st], out_cnt, err);
     }
 }
 
@@ -1212,9 +1255,8 @@ void slots_to_aos_launch(const Geo& g, BufView in, int which, double* out, unsig
 // ------------------------------------------------------------------------------
 // Host-side launchers
 // ------------------------------------------------------------------------------
-static size_t force_smem_bytes(int smax, int jpar, int maxh)
+static size_t force_smem_bytes(int smax, int /*jpar*/, int maxh)
 {
-    const int il = 32 / jpar;
     return (size_t)smax * (3 * sizeof(double) + 3 * sizeof(float)) +
            (size_t)(smax / 16 + 64 + 1) * sizeof(double4) + (size_t)maxh * FORCE_THREADS * sizeof(uint16_t);
 }
@@ -1336,6 +1378,13 @@ void signal_launch(uint32_t* flags, int first, int n, uint32_t value, cudaStream
 void energy_launch(const Geo& g, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s)
 {
     k_energy<<<nj, ENERGY_THREADS, 0, s>>>(g, stg, j0, e_out);
+}
+
+void drift_launch(const Geo& g, StgView stg, int j0, int nj, const UnitEnergy* e_out, int32_t* out_cnt,
+                  DevErr* err, cudaStream_t s)
+{
+    dim3 grid((unsigned)std::max(1, std::min((g.cap + DRIFT_THREADS - 1) / DRIFT_THREADS, 64)), (unsigned)nj);
+    k_drift<<<grid, DRIFT_THREADS, 0, s>>>(g, stg, j0, e_out, out_cnt, err);
 }
 
 void bin_scan_launch(const Geo& g, BufView out, int m0, int nm, DevErr* err, cudaStream_t s)

@@ -62,6 +62,11 @@ class dsea_energy(ctypes.Structure):
                 ("V", ctypes.c_double)]
 
 
+class dsea_profile(ctypes.Structure):
+    _fields_ = [("samples", ctypes.c_int64), ("n_sum", ctypes.c_double), ("U_sum", ctypes.c_double),
+                ("V_sum", ctypes.c_double), ("KE_sum", ctypes.c_double)]
+
+
 class dsea_stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_int64), ("force_launches", ctypes.c_int64),
                 ("atom_steps", ctypes.c_int64), ("force_ms", ctypes.c_double),
@@ -94,6 +99,9 @@ SIGNATURES = [
     ("dsea_get_cells", _st, [_c, _pi32, _pi32, ctypes.c_int64]),
     ("dsea_get_energies", _st, [_c, ctypes.POINTER(dsea_energy), ctypes.c_int64, _pi64]),
     ("dsea_set_state", _st, [_c, _pd, _pd, _pd, ctypes.c_int64]),
+    ("dsea_set_thermostat", _st, [_c, ctypes.c_int32, ctypes.c_double]),
+    ("dsea_get_profiles", _st, [_c, ctypes.POINTER(dsea_profile), ctypes.c_int32]),
+    ("dsea_reset_profiles", _st, [_c]),
     ("dsea_set_timing", _st, [_c, ctypes.c_int32]),
     ("dsea_get_stats", _st, [_c, ctypes.POINTER(dsea_stats)]),
     ("dsea_reset_stats", _st, [_c]),
@@ -256,18 +264,43 @@ def dsea_get_cells(ctx, n_atoms):
     return cells, sl
 
 
-def dsea_get_energies(ctx, cap=1 << 22):
+_ENERGY_DT = np.dtype([("step", np.int64), ("U", np.float64), ("KE", np.float64), ("V", np.float64)])
+
+
+def dsea_get_energies(ctx):
+    """(steps[n], [n, 4] = {U, KE, V, E = U + KE}) of every timestep this rank computed."""
     n = ctypes.c_int64()
-    _check(ctx, lib.dsea_get_energies(ctx, None, 0, ctypes.byref(n)))
-    buf = (dsea_energy * cap)()
-    _check(ctx, lib.dsea_get_energies(ctx, buf, cap, ctypes.byref(n)))
-    arr = np.zeros((n.value, 4))
-    steps = np.zeros(n.value, dtype=np.int64)
-    for i in range(n.value):
-        e = buf[i]
-        steps[i] = e.step
-        arr[i] = (e.U, e.KE, e.V, e.U + e.KE)
-    return steps, arr
+    cap = 4096
+    while True:   # the C call writes min(cap, available): grow until it comes back short
+        rec = np.zeros(cap, dtype=_ENERGY_DT)
+        _check(ctx, lib.dsea_get_energies(ctx, rec.ctypes.data_as(ctypes.POINTER(dsea_energy)), cap,
+                                          ctypes.byref(n)))
+        if n.value < cap:
+            break
+        cap *= 4
+    rec = rec[:n.value]
+    arr = np.stack([rec["U"], rec["KE"], rec["V"], rec["U"] + rec["KE"]], axis=1) if n.value else np.zeros((0, 4))
+    return rec["step"].copy(), arr
+
+
+def dsea_set_thermostat(ctx, T_target):
+    """NVT per-slice isokinetic thermostat at T_target (None/0 -> off), Q23."""
+    on = T_target is not None and T_target != 0
+    _check(ctx, lib.dsea_set_thermostat(ctx, 1 if on else 0, float(T_target) if on else 0.0))
+
+
+_PROFILE_DT = np.dtype([("samples", np.int64), ("n_sum", np.float64), ("U_sum", np.float64),
+                        ("V_sum", np.float64), ("KE_sum", np.float64)])
+
+
+def dsea_get_profiles(ctx, n_slices):
+    rec = np.zeros(n_slices, dtype=_PROFILE_DT)
+    _check(ctx, lib.dsea_get_profiles(ctx, rec.ctypes.data_as(ctypes.POINTER(dsea_profile)), n_slices))
+    return rec
+
+
+def dsea_reset_profiles(ctx):
+    _check(ctx, lib.dsea_reset_profiles(ctx))
 
 
 def dsea_set_state(ctx, xyz, vxyz, fxyz=None):
@@ -360,6 +393,39 @@ class Engine:
 
     def set_state(self, xyz, v, f=None):
         dsea_set_state(self.ctx, xyz, v, f)
+
+    def set_thermostat(self, T_target):
+        dsea_set_thermostat(self.ctx, T_target)
+
+    def pressure(self):
+        """Per-timestep virial pressure p = rho T + 24 V / (3 Vol), T = 2 KE / (3 N)
+        (Alg. 1's V; reading Q24)."""
+        g = self.geometry
+        vol = g.b[0] * g.b[1] * g.b[2]
+        _, e = self.energies()
+        n = self.n_atoms
+        return (n / vol) * (2.0 * e[:, 1] / (3.0 * n)) + 24.0 * e[:, 2] / (3.0 * vol)
+
+    def raw_profiles(self):
+        return dsea_get_profiles(self.ctx, self.geometry.n_slices)
+
+    def profiles(self, raw=None):
+        """x-resolved time averages per slice (Q24): slice centre x, atom
+        count n, density rho, potential energy per atom u, temperature T, pressure p."""
+        g = self.geometry
+        r = self.raw_profiles() if raw is None else raw
+        vol = g.w * g.b[1] * g.b[2]
+        s = np.maximum(r["samples"], 1)
+        n = r["n_sum"] / s
+        ke, U, V = r["KE_sum"] / s, r["U_sum"] / s, r["V_sum"] / s
+        with np.errstate(invalid="ignore", divide="ignore"):
+            T = np.where(n > 0, 2.0 * ke / (3.0 * n), 0.0)
+            u = np.where(n > 0, U / n, 0.0)
+        return {"x": (np.arange(g.n_slices) + 0.5) * g.w, "n": n, "rho": n / vol, "u": u, "T": T,
+                "p": (n / vol) * T + 24.0 * V / (3.0 * vol), "samples": r["samples"]}
+
+    def reset_profiles(self):
+        dsea_reset_profiles(self.ctx)
 
     def stats(self):
         return dsea_get_stats(self.ctx)

@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--calls", type=int, default=1)
     ap.add_argument("--block", type=int, default=0, help="slices per stage (0 = auto)")
     ap.add_argument("--hop", default="peer", choices=["peer", "nccl"])
+    ap.add_argument("--thermo", type=float, default=0.0, help="NVT thermostat T (0 = NVE)")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     rank = int(os.environ["RANK"])
@@ -46,6 +47,8 @@ def main():
     e.slice(n_slices=c.n_slices, cells_per_slice_x=c.cells_per_slice_x, n_gpus=world, rank=rank,
             device=local, workers_per_gpu=a.workers, slices_per_stage=a.block)
     _log(rank, "sliced")
+    if a.thermo > 0:
+        e.set_thermostat(a.thermo)
     D.ring_connect(e.ctx, rank, world, a.hop)
     _log(rank, "connected")
     per = a.steps // a.calls
@@ -55,13 +58,16 @@ def main():
     steps, en = e.energies()
     _log(rank, "energies")
     allv = [None] * world
-    dist.all_gather_object(allv, (steps.tolist(), en.tolist()))
+    prof = e.raw_profiles()
+    dist.all_gather_object(allv, (steps.tolist(), en.tolist(),
+                                  np.stack([prof[k] for k in ("n_sum", "U_sum", "V_sum", "KE_sum")], 1).tolist()))
     _log(rank, "gathered")
     if rank == 0:
-        st = sorted((s, tuple(v)) for s_, v_ in allv for s, v in zip(s_, v_))
+        st = sorted((s, tuple(v)) for s_, v_, _ in allv for s, v in zip(s_, v_))
+        prof_sum = np.sum([np.array(p_) for _, _, p_ in allv], axis=0)
         np.savez(a.out, x=e.positions(), v=e.velocities(), f=e.forces(),
                  steps=np.array([s for s, _ in st]), en=np.array([v for _, v in st]),
-                 stats=np.array([e.stats().hop_bytes]))
+                 stats=np.array([e.stats().hop_bytes]), prof=prof_sum)
     dist.barrier()
     D.ring_disconnect(e.ctx, world)
     e.close()

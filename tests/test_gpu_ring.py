@@ -17,29 +17,36 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _ngpus():
+    """GPUs on this box, counted in a subprocess: independent of what this pytest
+    process has already initialised (libdsea's static cudart, torch)."""
     try:
-        import torch
-        return torch.cuda.device_count()
+        r = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True, timeout=60)
+        return sum(1 for line in r.stdout.splitlines() if line.startswith("GPU "))
     except Exception:
         return 0
 
 
-def _single(cfg, steps):
+def _single(cfg, steps, thermo=0.0):
     c = CONFIGS[cfg]
     e = D.Engine(D.Box(c.nx, c.ny, c.nz, c.rho, c.rc, c.dt, c.T0, c.seed))
     e.slice(n_slices=c.n_slices, cells_per_slice_x=c.cells_per_slice_x)
+    if thermo:
+        e.set_thermostat(thermo)
     e.step(steps)
-    r = (e.positions(), e.velocities(), e.forces(), *e.energies())
+    p = e.raw_profiles()
+    r = (e.positions(), e.velocities(), e.forces(), *e.energies(),
+         np.stack([p[k] for k in ("n_sum", "U_sum", "V_sum", "KE_sum")], 1))
     e.close()
     return r
 
 
-def _ring(tmp_path, n, cfg, steps, workers=1, calls=1, block=0, hop="peer"):
-    out = str(tmp_path / f"ring_{n}_{cfg}_{steps}_{workers}_{calls}_{block}_{hop}.npz")
+def _ring(tmp_path, n, cfg, steps, workers=1, calls=1, block=0, hop="peer", thermo=0.0):
+    out = str(tmp_path / f"ring_{n}_{cfg}_{steps}_{workers}_{calls}_{block}_{hop}_{thermo}.npz")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={29500 + n * 7 + steps}",
            os.path.join(ROOT, "tests", "ring_worker.py"), "--config", cfg, "--steps", str(steps),
-           "--workers", str(workers), "--calls", str(calls), "--block", str(block), "--hop", hop, "--out", out]
+           "--workers", str(workers), "--calls", str(calls), "--block", str(block), "--hop", hop,
+           "--thermo", str(thermo), "--out", out]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return np.load(out)
@@ -60,7 +67,7 @@ def test_ring_bitwise_equals_single_gpu(tmp_path, n, cfg, steps, workers, calls,
     c = CONFIGS[cfg]
     if c.n_slices < 2 + 2 * workers:
         pytest.skip("too few slices")
-    x, v, f, s1, e1 = _single(cfg, steps)
+    x, v, f, s1, e1, _ = _single(cfg, steps)
     r = _ring(tmp_path, n, cfg, steps, workers, calls, block, hop)
     assert np.array_equal(r["x"], x)
     assert np.array_equal(r["v"], v)
@@ -68,3 +75,19 @@ def test_ring_bitwise_equals_single_gpu(tmp_path, n, cfg, steps, workers, calls,
     assert r["steps"].tolist() == list(range(steps))
     assert np.array_equal(r["en"], e1)
     assert int(r["stats"][0]) > 0  # slices really crossed NVLink
+
+
+@pytest.mark.parametrize("n,workers,block,hop", [(2, 1, 0, "peer"), (2, 2, 1, "nccl"), (4, 1, 0, "peer")])
+def test_ring_thermostat_bitwise_equals_single_gpu(tmp_path, n, workers, block, hop):
+    """NVT (per-slice isokinetic scaling, Q23) needs no exchange beyond the
+    ring hop: every rank scales the slices it processes, so the ring still equals
+    the single-GPU run bit for bit; x-resolved sums agree over ranks (Q24)."""
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    x, v, f, s1, e1, p1 = _single("P8", 12, thermo=1.5)
+    r = _ring(tmp_path, n, "P8", 12, workers, 1, block, hop, thermo=1.5)
+    assert np.array_equal(r["x"], x)
+    assert np.array_equal(r["v"], v)
+    assert np.array_equal(r["f"], f)
+    assert np.array_equal(r["en"], e1)
+    assert np.allclose(r["prof"], p1, rtol=1e-12, atol=0)
