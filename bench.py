@@ -198,6 +198,8 @@ def main():
     ap.add_argument("--hop", default="peer", choices=["peer", "nccl"],
                     help="ring hop: fused NVLink remote stores (peer) or NCCL send/recv")
     ap.add_argument("--block", type=int, default=0, help="slices per stage (0 = auto)")
+    ap.add_argument("--thermostat", type=float, default=0.0,
+                    help="NVT per-slice isokinetic thermostat at this T (P:314-316; 0 = NVE, the default)")
     args = ap.parse_args()
 
     from paper_2507_11289_b200 import CONFIGS
@@ -224,6 +226,8 @@ def main():
     e = D.Engine(D.Box(cfg.nx, cfg.ny, cfg.nz, cfg.rho, cfg.rc, cfg.dt, cfg.T0, cfg.seed))
     e.slice(n_slices=cfg.n_slices, cells_per_slice_x=cfg.cells_per_slice_x, n_gpus=world, rank=rank,
             device=local_rank, workers_per_gpu=W, slices_per_stage=args.block)
+    if args.thermostat > 0:
+        e.set_thermostat(args.thermostat)
     if world > 1:
         D.ring_connect(e.ctx, rank, world, args.hop)
     geo = e.geometry
@@ -327,6 +331,7 @@ def main():
             "config": {"workload": cfg.name, "n_atoms": atoms, "n_slices": geo.n_slices,
                        "cells": list(geo.cells), "rho": cfg.rho, "rc": cfg.rc, "dt": cfg.dt,
                        "workers_per_gpu": W, "timesteps_per_step": nw,
+                       "ensemble": f"NVT(T={args.thermostat})" if args.thermostat > 0 else "NVE",
                        "mode": "fused" if world == 1 and W == 1 else "staged-ring",
                        "l2": "inputs larger than L2 (state %.2f GB)" % (atoms * 76 / 1e9),
                        "parallelism": f"ring{world}", "ring_hop": args.hop if world > 1 else None},
@@ -335,7 +340,8 @@ def main():
                          "traffic": (None if traffic_pa is None else traffic_pa * atoms_per_launch),
                          "traffic_note": "dram read+write bytes per launch: ncu per-atom figure "
                                          "(profiles/r*/force_traffic.json) x atoms per launch",
-                         "kernel": "k_force (force + kick + drift + migration key)",
+                         "kernel": "k_force_pipe (force + kick + drift + migration key; NVT: "
+                                   "force + kick, drift in k_drift)",
                          "peak_note": f"FP64: {N_SMS} SMs x {FP64_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz",
                          "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
                                  "frac": hbm_achieved / hbm_peak, "peak_kind": peak_kind,

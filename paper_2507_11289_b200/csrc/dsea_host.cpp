@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -81,6 +82,24 @@ PFN_waitValue32 wait_value32()
         if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             f = reinterpret_cast<PFN_waitValue32>(p);
+    }
+    return f;
+}
+
+// cuStreamWriteValue32 (same route): publishes a ring-hop flag from the copy stream
+// without an SM, so it is not queued behind the persistent force kernel
+typedef int (*PFN_writeValue32)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+PFN_writeValue32 write_value32()
+{
+    static PFN_writeValue32 f = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            f = reinterpret_cast<PFN_writeValue32>(p);
     }
     return f;
 }
@@ -215,8 +234,12 @@ struct dsea_ctx {
     unsigned long long* count_dev = nullptr;
     unsigned long long tile_ctr_base = 0;
     std::vector<cudaEvent_t> ev_recv, ev_free, ev_bin, ev_send;
-    std::vector<cudaEvent_t> ev_force, ev_energy;   // per worker: force done / energies done
+    std::vector<cudaEvent_t> ev_force;              // per worker: force done
+    std::vector<cudaEvent_t> ev_energy;             // per (worker, block): energies of the block reduced
     std::vector<cudaEvent_t> ev_binblk;             // per block: last remote bin run done
+    std::vector<cudaEvent_t> ev_hop;                // per block: copy-engine hop of the last run done
+    std::vector<char> hop_rec;                      // ev_hop[k] has been recorded
+    bool ce_hop = false;                            // peer hop: local bin + copy engine (default)
     cudaEvent_t ev_cs = nullptr;                    // compute-stream point for the bin stream
 
     bool connected = false;
@@ -382,6 +405,7 @@ void disconnect(dsea_ctx* c)
         if (c->pred_rel) cudaIpcCloseMemHandle(c->pred_rel);
         c->succ_in_base = nullptr; c->succ_arr = nullptr; c->pred_rel = nullptr;
         c->peer = false;
+        c->ce_hop = false;
         if (!c->outb.empty() && c->outb.back().remote) {
             c->outb.back().base = c->own_outb_last;
             c->outb.back().remote = 0;
@@ -424,6 +448,9 @@ void free_device(dsea_ctx* c)
     if (c->bs) cudaStreamDestroy(c->bs);
     for (cudaEvent_t e : c->ev_binblk) cudaEventDestroy(e);
     c->ev_binblk.clear();
+    for (cudaEvent_t e : c->ev_hop) cudaEventDestroy(e);
+    c->ev_hop.clear();
+    c->hop_rec.clear();
     if (c->ev_cs) cudaEventDestroy(c->ev_cs);
     c->ev_cs = nullptr;
     c->bs = nullptr;
@@ -647,9 +674,13 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 }
             }
             cudaEvent_t t0 = nullptr, t1 = nullptr;
-            // the previous per-atom energy records of this worker must be reduced first
-            if (c->T.pipe) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_energy[w], 0));
-            if (c->peer && w == W - 1) {
+            // this block's per-atom energy records of the previous super-cycle must be
+            // reduced before the pass rewrites them (other blocks' reductions may still
+            // run: they overlap this pass instead of stalling it)
+            const int nblk_e = (ns + c->B - 1) / c->B;
+            cudaEvent_t& ev_e = c->ev_energy[(size_t)w * nblk_e + (j / c->B) % nblk_e];
+            if (c->T.pipe) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, ev_e, 0));
+            if (c->peer && !c->ce_hop && w == W - 1) {
                 // staging of this block and the arrival counters it adds to were last read
                 // by the remote bin runs of blocks c and c+1 one super-cycle ago
                 const int nblk = (ns + c->B - 1) / c->B;
@@ -665,13 +696,13 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 UnitEnergy* eo = c->e_dev + (size_t)op.t_rel * ns;
                 energy_launch(c->g, c->stg[w], j, n, eo, c->cs);
                 drift_launch(c->g, c->stg[w], j, n, eo, c->outb[w].cnt, c->err_dev, c->cs);
-                CUDA_TRY(c, cudaEventRecord(c->ev_energy[w], c->cs));
+                CUDA_TRY(c, cudaEventRecord(ev_e, c->cs));
                 c->stats.kernel_launches += 2;
             } else if (c->T.pipe) {  // per-slice energy reduction off the critical path
                 CUDA_TRY(c, cudaEventRecord(c->ev_force[w], c->cs));
                 CUDA_TRY(c, cudaStreamWaitEvent(c->es, c->ev_force[w], 0));
                 energy_launch(c->g, c->stg[w], j, n, c->e_dev + (size_t)op.t_rel * ns, c->es);
-                CUDA_TRY(c, cudaEventRecord(c->ev_energy[w], c->es));
+                CUDA_TRY(c, cudaEventRecord(ev_e, c->es));
                 c->stats.kernel_launches++;
             }
             if (w == 0 && c->NG > 1) {
@@ -714,9 +745,9 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 }
             }
             BufView& src = in_of(w);
-            BufView& dst = c->outb[w];
-            if (src.base != dst.base)
-                CUDA_TRY(c, cudaMemcpyAsync(dst.base + (size_t)j * sb, src.base + (size_t)j * sb, sb * n,
+            char* dst_base = (c->ce_hop && w == W - 1 && c->NG > 1) ? c->succ_in_base : c->outb[w].base;
+            if (src.base != dst_base)
+                CUDA_TRY(c, cudaMemcpyAsync(dst_base + (size_t)j * sb, src.base + (size_t)j * sb, sb * n,
                                             cudaMemcpyDeviceToDevice, c->cs));
             if (w == 0 && c->NG > 1) {
                 if (c->peer) {
@@ -735,6 +766,44 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
         }
         case OP_BIN: {
             const int m = op.slice, n = op.count, w = op.worker;
+            if (c->ce_hop && w == W - 1 && c->NG > 1) {
+                // copy-engine hop: bin into the local last buffer on the compute stream,
+                // then the copy stream pushes the finished slots over NVLink and raises
+                // the successor's arrival flags -- neither needs an SM, so both overlap
+                // the next block's (persistent, SM-filling) force pass
+                const int nblk = (ns + c->B - 1) / c->B;
+                for (int k = m / c->B; k <= (m + n - 1) / c->B; k++)   // previous push of these slots
+                    if (c->hop_rec[k % nblk]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_hop[k % nblk], 0));
+                cudaEvent_t t0 = nullptr, t1 = nullptr;
+                if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
+                const int s0 = std::max(m - 1, 0), s1 = std::min(m + n, ns - 1);
+                BufView& ob = c->outb[w];
+                bin_scan_launch(c->g, ob, m, n, c->err_dev, c->cs);
+                bin_place_launch(c->g, ob, c->stg[w], s0, s1 - s0 + 1, 0, m, n, c->err_dev, c->cs);
+                bin_gather_launch(c->g, ob, c->stg[w], m, n, c->err_dev, c->cs);
+                c->stats.kernel_launches += 3;
+                if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_BIN, {t0, t1}}); }
+                const uint32_t wv = ++c->wr_cnt[m];
+                for (int sl = m + 1; sl < m + n; sl++) c->wr_cnt[sl] = wv;
+                CUDA_TRY(c, cudaEventRecord(c->ev_cs, c->cs));
+                CUDA_TRY(c, cudaStreamWaitEvent(c->bs, c->ev_cs, 0));
+                for (int sl = m; sl < m + n; sl++)   // the successor released the previous occupants
+                    if (wait_value32()(c->bs, (unsigned long long)(c->rel_dev + sl), wv, 0))
+                        return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (release) failed");
+                cudaEvent_t h0 = nullptr, h1 = nullptr;
+                if (c->timing) { h0 = tev(c); h1 = tev(c); cudaEventRecord(h0, c->bs); }
+                CUDA_TRY(c, cudaMemcpyAsync(c->succ_in_base + (size_t)m * sb, ob.base + (size_t)m * sb, sb * n,
+                                            cudaMemcpyDeviceToDevice, c->bs));
+                for (int sl = m; sl < m + n; sl++)
+                    if (write_value32()(c->bs, (unsigned long long)(c->succ_arr + sl), wv, 0))
+                        return fail(c, DSEA_EPEER, "cuStreamWriteValue32 (arrival) failed");
+                if (c->timing) { cudaEventRecord(h1, c->bs); c->tpairs.push_back({TK_SEND, {h0, h1}}); }
+                const int key = ((m + n - 1) / c->B) % nblk;
+                CUDA_TRY(c, cudaEventRecord(c->ev_hop[key], c->bs));
+                c->hop_rec[key] = 1;
+                c->stats.hop_bytes += (int64_t)sb * n;
+                break;
+            }
             uint32_t wv = 0;
             // the last worker's bins write into the successor over NVLink: run them on
             // their own stream so the transfer overlaps the next block's force pass
@@ -1027,13 +1096,14 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
         const int nblk = (g.ns + c->B - 1) / c->B;
         c->ev_binblk.resize(nblk);
         for (int k = 0; k < nblk; k++) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_binblk[k], cudaEventDisableTiming));
+        c->ev_hop.resize(nblk);
+        for (int k = 0; k < nblk; k++) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_hop[k], cudaEventDisableTiming));
+        c->hop_rec.assign(nblk, 0);
     }
     c->ev_force.resize(c->W);
-    c->ev_energy.resize(c->W);
-    for (int w = 0; w < c->W; w++) {
-        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_force[w], cudaEventDisableTiming));
-        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_energy[w], cudaEventDisableTiming));
-    }
+    for (int w = 0; w < c->W; w++) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_force[w], cudaEventDisableTiming));
+    c->ev_energy.resize((size_t)c->W * ((g.ns + c->B - 1) / c->B));
+    for (auto& e : c->ev_energy) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto* v : {&c->ev_recv, &c->ev_free, &c->ev_bin, &c->ev_send}) {
         v->resize(g.ns);
         for (int j = 0; j < g.ns; j++) CUDA_TRY(c, cudaEventCreateWithFlags(&(*v)[j], cudaEventDisableTiming));
@@ -1131,11 +1201,19 @@ dsea_status dsea_ring_connect_peer(dsea_ctx* c, const void* blobs, size_t blob_b
     c->wr_cnt.assign(ns, 0u);
     c->exp_arr.assign(ns, 0u);
     c->rel_cnt.assign(ns, c->rank == 0 ? 0u : 1u);
-    // the last worker's output buffer is the successor's input buffer (local scratch kept)
-    BufView& last = c->outb[c->W - 1];
-    c->own_outb_last = last.base;
-    last.base = c->succ_in_base;
-    last.remote = 1;
+    // hop: copy engine (default; local bin + cudaMemcpyAsync over NVLink + flag write)
+    // or SM remote stores (DSEA_PEER_HOP=sm: the bin kernels write the successor's slots)
+    const char* hop = getenv("DSEA_PEER_HOP");
+    c->ce_hop = !(hop && std::strcmp(hop, "sm") == 0);
+    if (c->ce_hop && !write_value32()) return fail(c, DSEA_EPEER, "cuStreamWriteValue32 unavailable");
+    if (!c->ce_hop) {
+        // the last worker's output buffer is the successor's input buffer (local scratch kept)
+        BufView& last = c->outb[c->W - 1];
+        c->own_outb_last = last.base;
+        last.base = c->succ_in_base;
+        last.remote = 1;
+    }
+    std::fill(c->hop_rec.begin(), c->hop_rec.end(), 0);
     CUDA_TRY(c, cudaDeviceSynchronize());
     c->connected = true;
     return DSEA_OK;
