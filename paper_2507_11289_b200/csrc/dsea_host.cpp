@@ -486,7 +486,7 @@ dsea_status alloc_buf(dsea_ctx* c, BufView* B)
     if ((s = dalloc(c, &B->perm, (size_t)c->g.ns * c->g.cap))) return s;
     CUDA_TRY(c, cudaMemset(B->cnt, 0, sizeof(int32_t) * (size_t)c->g.ns * c->g.ncell));
     // zeroed scratch: after a reported error no later pass can index out of bounds
-    CUDA_TRY(c, cudaMemset(B->perm, 0, sizeof(int32_t) * (size_t)c->g.ns * c->g.cap));
+    CUDA_TRY(c, cudaMemset(B->perm, 0, sizeof(BinRec) * (size_t)c->g.ns * c->g.cap));
     CUDA_TRY(c, cudaMemset(B->base, 0, c->L.slot_bytes * (size_t)c->g.ns));
     return DSEA_OK;
 }
@@ -1043,6 +1043,11 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     g.ncell = g.c * geo.cells[1] * geo.cells[2];
     g.cap = geo.slot_capacity;
     g.rc2_screen = (float)(g.rc2 * (1.0 + 1e-5) + 1e-3);
+    {   // gather rows: about twice the mean cell occupancy (rarer larger cells: global path)
+        const double mean_cell = (double)c->N / ((double)g.ns * g.ncell);
+        g.cell_max = 32;
+        while (g.cell_max < 128 && g.cell_max < 2.0 * mean_cell + 24.0) g.cell_max *= 2;
+    }
     g.thermo = 0;          // NVE until dsea_set_thermostat
     g.T_target = 0.0;
     c->L = make_slot_layout(g.ncell, g.cap);

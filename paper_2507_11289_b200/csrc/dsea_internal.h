@@ -30,6 +30,7 @@ struct Geo {
     int ncell;      // cells per slice = c * cells[1] * cells[2]
     int cap;        // atoms per slot
     float rc2_screen;  // fp32 pre-screen radius^2 (rc^2 + margin)
+    int cell_max;      // k_bin_gather shared-memory rows per cell (larger cells: global path)
     int thermo;        // NVT: per-slice isokinetic scaling before the drift (Q23)
     double T_target;   // thermostat temperature
 };
@@ -59,11 +60,18 @@ inline SlotLayout make_slot_layout(int ncell, int cap) {
 }
 
 // Device view of a slot buffer.
+// Bin record of one arrival: written by k_bin_place, ranked and gathered by k_bin_gather.
+struct BinRec {
+    double z;        // position z (first sort key, Q21)
+    int32_t src;     // staging index
+    int32_t id;      // atom id (second sort key)
+};
+
 struct BufView {
     char* base;
     SlotLayout L;
     int32_t* cnt;    // [ns*ncell] per-cell arrival counters / cursors (not sent)
-    int32_t* perm;   // [ns*cap] bin scratch (not sent)
+    BinRec* perm;    // [ns*cap] bin scratch (not sent)
     int remote;      // slots live in the ring successor's memory (peer backend)
 };
 

@@ -1114,24 +1114,35 @@ k_bin_place(Geo g, BufView out, StgView stg, int s0, int flat_count, int m0, int
     if (m < m0 || m >= m0 + nm) return;
     const int c = key - m * g.ncell;
     const int pos = atomicAdd(&out.cnt[(size_t)m * g.ncell + c], 1);
-    if (pos < g.cap) out.perm[(size_t)m * g.cap + pos] = base + p;
+    if (pos < g.cap) {
+        // the sort keys travel with the index (coalesced reads here), so the gather
+        // ranks a cell without a dependent round trip to staging
+        BinRec r;
+        r.z = stg.z[base + p];
+        r.src = base + p;
+        r.id = stg.id[base + p];
+        out.perm[(size_t)m * g.cap + pos] = r;
+    }
 }
 
 // ------------------------------------------------------------------------------
-// Bin pass 3: one half-warp per cell (cells hold ~13 atoms at rho 0.8) sorts its
-// arrivals by (z, id) -- a data-determined order, identical for every schedule --
-// and gathers them from staging into the slot; resets the cell's counter.
+// Bin pass 3: one half-warp per cell (cells hold ~13 atoms at rho 0.8, rc 2.5)
+// ranks its arrivals by (z, id) -- a data-determined order, identical for every
+// schedule -- and gathers them from staging into the slot; resets the cell's
+// counter.  The records (z, src, id) come from k_bin_place; up to CM per cell are
+// ranked in shared memory (rows padded against bank conflicts between the two
+// half-warps), larger cells straight from the records in global memory.
 // ------------------------------------------------------------------------------
 constexpr int GATHER_THREADS = 256;
 constexpr int GATHER_CELLS = GATHER_THREADS / 16;   // cells per CTA
-constexpr int CELL_MAX = 128;
 
+template <int CM>
 __global__ void __launch_bounds__(GATHER_THREADS)
-k_bin_gather(Geo g, BufView out, StgView stg, int m0, DevErr* err)
+k_bin_gather(Geo g, BufView out, StgView stg, int m0)
 {
-    __shared__ double kz[GATHER_CELLS][CELL_MAX];
-    __shared__ int kid[GATHER_CELLS][CELL_MAX];
-    __shared__ int ksrc[GATHER_CELLS][CELL_MAX];
+    __shared__ double kz[GATHER_CELLS][CM + 1];
+    __shared__ int kid[GATHER_CELLS][CM + 1];
+    __shared__ int ksrc[GATHER_CELLS][CM + 1];
     const int sub = threadIdx.x & 15, hw = threadIdx.x >> 4;
     const unsigned hmask = 0xffffu << (threadIdx.x & 16);
     const int m = m0 + blockIdx.y;
@@ -1142,17 +1153,7 @@ k_bin_gather(Geo g, BufView out, StgView stg, int m0, DevErr* err)
     if (sub == 0) out.cnt[(size_t)m * g.ncell + c] = 0;
     if (cs[g.ncell] > g.cap) return;  // capacity error already flagged by the scan
     const int n = en - st;
-    if (n > CELL_MAX) {
-        if (sub == 0) set_err(err, DSEA_ECAPACITY, m, -1, n);
-        return;
-    }
-    for (int e = sub; e < n; e += 16) {
-        const int src = out.perm[(size_t)m * g.cap + st + e];
-        ksrc[hw][e] = src;
-        kz[hw][e] = stg.z[src];
-        kid[hw][e] = stg.id[src];
-    }
-    __syncwarp(hmask);
+    const BinRec* R = out.perm + (size_t)m * g.cap + st;
     double* ox = slot_d(out, m, out.L.off_x);
     double* oy = slot_d(out, m, out.L.off_y);
     double* oz = slot_d(out, m, out.L.off_z);
@@ -1163,20 +1164,41 @@ k_bin_gather(Geo g, BufView out, StgView stg, int m0, DevErr* err)
     double* ofy = slot_d(out, m, out.L.off_fy);
     double* ofz = slot_d(out, m, out.L.off_fz);
     int32_t* oid = slot_i(out, m, out.L.off_id);
-    for (int e = sub; e < n; e += 16) {
-        const double z = kz[hw][e];
-        const int id = kid[hw][e];
-        int rank = 0;
-        for (int e2 = 0; e2 < n; e2++) {
-            const double z2 = kz[hw][e2];
-            rank += (z2 < z) || (z2 == z && kid[hw][e2] < id);
-        }
-        const int src = ksrc[hw][e];
+    auto put = [&](int src, double z, int id, int rank) {
         const int d = st + rank;
         ox[d] = stg.x[src]; oy[d] = stg.y[src]; oz[d] = z;
         ovx[d] = stg.vx[src]; ovy[d] = stg.vy[src]; ovz[d] = stg.vz[src];
         ofx[d] = stg.fx[src]; ofy[d] = stg.fy[src]; ofz[d] = stg.fz[src];
         oid[d] = id;
+    };
+    if (n <= CM) {
+        for (int e = sub; e < n; e += 16) {
+            const BinRec r = R[e];
+            ksrc[hw][e] = r.src;
+            kz[hw][e] = r.z;
+            kid[hw][e] = r.id;
+        }
+        __syncwarp(hmask);
+        for (int e = sub; e < n; e += 16) {
+            const double z = kz[hw][e];
+            const int id = kid[hw][e];
+            int rank = 0;
+            for (int e2 = 0; e2 < n; e2++) {
+                const double z2 = kz[hw][e2];
+                rank += (z2 < z) || (z2 == z && kid[hw][e2] < id);
+            }
+            put(ksrc[hw][e], z, id, rank);
+        }
+    } else {
+        for (int e = sub; e < n; e += 16) {
+            const BinRec r = R[e];
+            int rank = 0;
+            for (int e2 = 0; e2 < n; e2++) {
+                const BinRec r2 = R[e2];
+                rank += (r2.z < r.z) || (r2.z == r.z && r2.id < r.id);
+            }
+            put(r.src, r.z, r.id, rank);
+        }
     }
     if (out.remote) __threadfence_system();
 }
@@ -1408,8 +1430,11 @@ void bin_place_launch(const Geo& g, BufView out, StgView stg, int s0, int nsrc, 
 void bin_gather_launch(const Geo& g, BufView out, StgView stg, int m0, int nm, DevErr* err,
                        cudaStream_t s)
 {
+    (void)err;
     dim3 grid((g.ncell + GATHER_CELLS - 1) / GATHER_CELLS, nm);
-    k_bin_gather<<<grid, GATHER_THREADS, 0, s>>>(g, out, stg, m0, err);
+    if (g.cell_max <= 32) k_bin_gather<32><<<grid, GATHER_THREADS, 0, s>>>(g, out, stg, m0);
+    else if (g.cell_max <= 64) k_bin_gather<64><<<grid, GATHER_THREADS, 0, s>>>(g, out, stg, m0);
+    else k_bin_gather<128><<<grid, GATHER_THREADS, 0, s>>>(g, out, stg, m0);
 }
 
 void init_keys_launch(const Geo& g, StgView stg, int n, int32_t* out_cnt, DevErr* err,
