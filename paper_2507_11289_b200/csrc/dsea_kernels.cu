@@ -605,7 +605,7 @@ size_t pipe_smem_bytes(int smax, int maxh)
     return 2 * per + (size_t)maxh * PIPE_CT * sizeof(uint16_t);
 }
 
-template <int JPAR>
+template <int JPAR, bool NVT>
 __global__ void __launch_bounds__(PIPE_THREADS, PIPE_MINB)
 k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt, int j0, int nj,
              DevErr* __restrict__ err, unsigned long long* __restrict__ tile_ctr,
@@ -966,7 +966,7 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                 const double ke2 = vx * vx + vy * vy + vz * vz;
                 const size_t st = (size_t)j * g.cap + gi;
                 stg.eatom[st] = make_double4(e_u, e_v, ke2, (double)e_np);
-                if (g.thermo) {
+                if (NVT) {
                     // NVT: the slice's scale factor needs every atom's kick first
                     // (k_energy -> lambda_j, then k_drift finishes md_v3b)
                     stg.x[st] = xi; stg.y[st] = yi; stg.z[st] = zi;
@@ -1284,8 +1284,7 @@ static size_t force_smem_bytes(int smax, int /*jpar*/, int maxh)
 }
 
 
-static size_t pipe_smem_attr = 0;    // largest dynamic smem set on k_force_pipe<2> so far
-static size_t pipe_smem_attr4 = 0;   // ... on k_force_pipe<4>
+static size_t pipe_smem_attr = 0;    // largest dynamic smem set on k_force_pipe so far
 
 static double env_num(const char* name, double dflt)
 {
@@ -1317,7 +1316,7 @@ Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
     T.tiles = g.c * g.cells[1] * T.nzt;
     T.pipe = env_num("DSEA_FORCE_V2", 0) == 0;
     if (T.pipe) {
-        T.jpar = (int)env_num("DSEA_PIPE_JPAR", 2) == 4 ? 4 : 2;
+        T.jpar = 2;
         T.nzt = std::max(1, (int)std::ceil(1.25 * mean_col / PIPE_HOME) + 1);
         T.tiles = g.c * g.cells[1] * T.nzt;
         const double per_col_p = std::min(mean_col + 2.0 * mean_per_cell,
@@ -1335,15 +1334,19 @@ int force_kernel_attr(const Tiling& T)
 {
     if (T.pipe) {
         // the attribute is process-wide: keep the largest request of any context
-        auto kern = T.jpar == 4 ? k_force_pipe<4> : k_force_pipe<2>;
-        size_t& attr = T.jpar == 4 ? pipe_smem_attr4 : pipe_smem_attr;
-        if (T.smem > attr) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem);
+        if (T.smem > pipe_smem_attr) {
+            cudaError_t e = cudaFuncSetAttribute(k_force_pipe<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)T.smem);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k_force_pipe<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)T.smem);
             if (e != cudaSuccess) return -1;
-            attr = T.smem;
+            pipe_smem_attr = T.smem;
         }
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PIPE_THREADS, T.smem);
+        int per_sm = 0, per_sm_nvt = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force_pipe<2, false>, PIPE_THREADS, T.smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_nvt, k_force_pipe<2, true>, PIPE_THREADS, T.smem);
+        per_sm = std::min(per_sm, per_sm_nvt);   // one grid size serves both instantiations
         if (per_sm < 1) return -1;
         return per_sm;
     }
@@ -1360,12 +1363,14 @@ int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t
     if (T.pipe) {
         // the tile counter is never reset: each launch consumes exactly ntiles + grid
         // increments, so the host tracks the base of every launch
-        if (T.jpar == 4)
-            k_force_pipe<4><<<T.grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err,
-                                                                 T.ctr, *T.ctr_base);
+        // NVE: force + kick + drift + destination in one pass; NVT: force + kick (the
+        // drift needs the slice's lambda, k_drift)
+        if (g.thermo)
+            k_force_pipe<2, true><<<T.grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err,
+                                                                       T.ctr, *T.ctr_base);
         else
-            k_force_pipe<2><<<T.grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err,
-                                                                 T.ctr, *T.ctr_base);
+            k_force_pipe<2, false><<<T.grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err,
+                                                                        T.ctr, *T.ctr_base);
         *T.ctr_base += (unsigned long long)nj * T.tiles + T.grid;
         return 1;
     }

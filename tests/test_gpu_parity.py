@@ -275,3 +275,22 @@ def test_error_paths():
         D.dsea_step(ctx, 1)
     assert ei.value.status == D.DSEA_ESTATE
     D.dsea_destroy(ctx)
+
+
+def test_overfull_cell_binned_exactly():
+    """A cell far above its expected occupancy (100 atoms where ~18 are typical) is
+    ranked by k_bin_gather's global-memory path: positions round-trip exactly by id,
+    every cell is bit-exact against the oracle's binning, and a step runs on it."""
+    e, c = _engine("C1")
+    g = _geom(c)
+    x = oracle.lattice(c.nx, c.ny, c.nz, g.a)
+    rng = np.random.default_rng(3)
+    lo = np.array([2, 2, 2]) * g.l
+    idx = rng.choice(c.n_atoms, 100, replace=False)
+    x[idx] = lo + rng.random((100, 3)) * g.l * 0.999
+    v = np.zeros_like(x)
+    e.set_state(x, v)
+    assert np.array_equal(e.positions(), x)
+    _cells_exact(e, c)
+    cg, _ = e.cells()
+    assert np.sum(np.all(cg == [2, 2, 2], axis=1)) >= 100
