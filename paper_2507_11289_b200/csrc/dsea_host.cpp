@@ -1266,6 +1266,9 @@ dsea_status dsea_step(dsea_ctx* c, int64_t n_steps)
     c->mirror_valid = false;
     c->tev_used = 0;
     c->tpairs.clear();
+    cudaEvent_t tl0 = nullptr;   // timeline origin (timing on and DSEA_TIMELINE set)
+    const char* tl_path = c->timing ? getenv("DSEA_TIMELINE") : nullptr;
+    if (tl_path) { tl0 = tev(c); cudaEventRecord(tl0, c->cs); }
     dsea_status s = c->mode == DSEA_MODE_FUSED ? run_fused(c, n_steps) : run_plan(c, n_steps);
     if (s) return s;
     CUDA_TRY(c, cudaStreamSynchronize(c->cs));
@@ -1277,13 +1280,28 @@ dsea_status dsea_step(dsea_ctx* c, int64_t n_steps)
     if ((s = check_dev_err(c))) return s;
 
     // timing
+    FILE* tl = nullptr;
+    if (tl0) {   // diagnostic timeline: one CSV per rank, intervals relative to the call start
+        char fn[512];
+        std::snprintf(fn, sizeof fn, "%s.rank%d.csv", tl_path, c->rank);
+        tl = std::fopen(fn, "w");
+        if (tl) std::fprintf(tl, "kind,start_ms,end_ms\n");
+    }
     for (auto& tp : c->tpairs) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, tp.second.first, tp.second.second);
         if (tp.first == TK_FORCE) c->stats.force_ms += ms;
         else if (tp.first == TK_BIN) c->stats.bin_ms += ms;
         else c->stats.hop_ms += ms;
+        if (tl) {
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, tl0, tp.second.first);
+            cudaEventElapsedTime(&b, tl0, tp.second.second);
+            std::fprintf(tl, "%s,%.4f,%.4f\n", tp.first == TK_FORCE ? "force" : tp.first == TK_BIN ? "bin" : "hop",
+                         a, b);
+        }
     }
+    if (tl) std::fclose(tl);
     c->tpairs.clear();
 
     // energies of the timesteps this rank computed, summed over slices in slice order
