@@ -1047,49 +1047,66 @@ k_drift(Geo g, StgView stg, int j0, const UnitEnergy* __restrict__ e_out, int32_
 // counters become cursors.  One CTA per slot.
 // ------------------------------------------------------------------------------
 constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;                        // counters per thread per chunk
+constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_ITEMS;
 
+// Chunks of SCAN_CHUNK counters: coalesced load into shared memory, each thread scans
+// SCAN_ITEMS consecutive ones, a block-wide scan of the thread sums, coalesced stores;
+// the running total carries over to the next chunk.
 __global__ void __launch_bounds__(SCAN_THREADS)
 k_bin_scan(Geo g, BufView out, int m0, DevErr* err)
 {
+    __shared__ int buf[SCAN_CHUNK];
+    __shared__ int wsum[32];
+    __shared__ int carry_s;
     const int m = m0 + blockIdx.x;
     int32_t* cnt = out.cnt + (size_t)m * g.ncell;
     int32_t* cs = slot_cs_w(out, m);
     const int n = g.ncell;
-    const int per = (n + SCAN_THREADS - 1) / SCAN_THREADS;
-    const int a = threadIdx.x * per, b = min(n, a + per);
-    int sum = 0;
-    for (int c = a; c < b; c++) sum += cnt[c];
-    __shared__ int wsum[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int incl = sum;
+    int carry = 0;
+    for (int c0 = 0; c0 < n; c0 += SCAN_CHUNK) {
+        const int len = min(SCAN_CHUNK, n - c0);
+        for (int i = threadIdx.x; i < SCAN_CHUNK; i += SCAN_THREADS) buf[i] = i < len ? cnt[c0 + i] : 0;
+        __syncthreads();
+        int v[SCAN_ITEMS];
+        int sum = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int v = __shfl_up_sync(FULLMASK, incl, o);
-        if (lane >= o) incl += v;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        int v = wsum[lane];
-        int iv = v;
+        for (int k = 0; k < SCAN_ITEMS; k++) { v[k] = buf[threadIdx.x * SCAN_ITEMS + k]; sum += v[k]; }
+        int incl = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int u = __shfl_up_sync(FULLMASK, iv, o);
-            if (lane >= o) iv += u;
+            const int u = __shfl_up_sync(FULLMASK, incl, o);
+            if (lane >= o) incl += u;
         }
-        wsum[lane] = iv - v;
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const int w = wsum[lane];
+            int iw = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(FULLMASK, iw, o);
+                if (lane >= o) iw += u;
+            }
+            wsum[lane] = iw - w;
+            if (lane == 31) carry_s = iw;   // chunk total
+        }
+        __syncthreads();
+        int run = carry + wsum[warp] + incl - sum;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; k++) { buf[threadIdx.x * SCAN_ITEMS + k] = run; run += v[k]; }
+        __syncthreads();
+        for (int i = threadIdx.x; i < len; i += SCAN_THREADS) {
+            cs[c0 + i] = buf[i];
+            cnt[c0 + i] = buf[i];
+        }
+        carry += carry_s;
+        __syncthreads();
     }
-    __syncthreads();
-    int run = wsum[warp] + incl - sum;
-    for (int c = a; c < b; c++) {
-        const int k = cnt[c];
-        cs[c] = run;
-        cnt[c] = run;
-        run += k;
-    }
-    if (threadIdx.x == SCAN_THREADS - 1) {
-        cs[n] = run;
-        if (run > g.cap) set_err(err, DSEA_ECAPACITY, m, -1, run);
+    if (threadIdx.x == 0) {
+        cs[n] = carry;
+        if (carry > g.cap) set_err(err, DSEA_ECAPACITY, m, -1, carry);
     }
     if (out.remote) __threadfence_system();
 }
