@@ -260,6 +260,17 @@ dsea_status dsea_geometry_compute(const dsea_box_params *box, const dsea_slice_p
 dsea_status dsea_schedule(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_t workers_per_gpu,
                           int32_t n_cycles, int32_t *rows, int64_t cap_rows, int64_t *n_rows);
 
+/* The op list one rank's runtime executes for n_steps timesteps with B =
+ * slices_per_stage slices per stage (the generalised Table 1 of dsea_schedule), in
+ * stream order.  Each row is 7 int32: {kind (0 recv, 1 force, 2 pass-through,
+ * 3 bin/finalise, 4 send), stage, worker (-1 for recv), first slice (0-based),
+ * slice count, super-cycle, timestep relative to the call (force; else -1)}.
+ * rows = NULL queries the count into *n_rows.  Host only; used by the CPU tests to
+ * check the cross-rank dependency order (no deadlock, every unit once). */
+dsea_status dsea_plan_ops(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_t workers_per_gpu,
+                          int64_t n_steps, int32_t slices_per_stage, int32_t *rows, int64_t cap_rows,
+                          int64_t *n_rows);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,6 +34,9 @@ CONFIGS = {
     "C3": Config("C3", 400, 40, 32, 256, note="2,048,000 atoms, 256 slices, 8-GPU ring"),
     "C4": Config("C4", 160, 160, 160, 0, note="16,384,000-atom cube, 109 slices (paper rule), "
                  "strong scaling 1/2/4/8 GPUs"),
+    "S12": Config("S12", 18, 64, 64, 12, note="294,912 atoms, 12 slices: Eq. (1) N_max = 3 (W=1), 2 (W=2); "
+                  "NEXT-2 scaling study"),
+    "S24": Config("S24", 36, 64, 64, 24, note="589,824 atoms, 24 slices: N_max = 6 (W=1), 4 (W=2), 3 (W=3)"),
     "C5a": Config("C5a", 400, 40, 32, 273, note="C3 box, rc 2.5, 1 cell/slice"),
     "C5b": Config("C5b", 400, 40, 32, 136, cells_per_slice_x=2, note="C3 box, rc 2.5, 2 cells/slice"),
     "C5c": Config("C5c", 400, 40, 32, 91, cells_per_slice_x=3, note="C3 box, rc 2.5, 3 cells/slice"),

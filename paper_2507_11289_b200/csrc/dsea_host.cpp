@@ -140,12 +140,22 @@ struct Plan {
     int n_stages = 0;
 };
 
+bool plan_plateau(int ns, int ng, int W, int B);
+int plan_gap(int ns, int ng, int W, int B);
+
 Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps, int B)
 {
     Plan P;
     if (B < 1) B = 1;
     const int nblk = (ns + B - 1) / B;
     const int d = (B == 1) ? 2 : 1;
+    // past Eq. (1)'s bound: close each super-cycle before the next (see plan_gap).
+    // With W > 1 the last slice is always finalised with its own block: worker w+1
+    // processes the previous block in the same stage and, when the last block is a
+    // single slice, needs it (found by tests/test_plan_sim.py).
+    const bool plateau = plan_plateau(ns, ng, W, B);
+    const bool early_fin = plateau || W > 1;
+    const int gap = plan_gap(ns, ng, W, B);
     const int64_t nw = (int64_t)ng * W;
     const int64_t n_cycles = n_steps <= 0 ? 0 : (n_steps + nw - 1) / nw;
     const int64_t items = n_cycles * nblk;
@@ -153,51 +163,97 @@ Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps, int B)
     auto active = [&](int64_t K, int w) { return K * nw + (int64_t)rank * W + w < n_steps; };
     auto blk_first = [&](int c) { return c * B; };
     auto blk_count = [&](int c) { return std::min(B, ns - c * B); };
-    int64_t r_lo = 0, r_hi = 0;  // flat blocks received at stage == block index
+    // stage of flat block p: receive at sp(p), worker w processes it at sp(p) + 2 + d*w,
+    // where sp(p) = p + gap * (p / nblk) (gap idle stages after each super-cycle)
+    auto sp = [&](int64_t p) { return p + (int64_t)gap * (p / nblk); };
+    int64_t r_lo = 0, r_hi = 0;  // flat blocks received
     if (ng > 1) {
         if (rank == 0) { r_lo = nblk; r_hi = items + nblk; }
         else { r_lo = 0; r_hi = items; }
     }
-    const int64_t last_compute = items + 2 + (int64_t)d * (W - 1);  // finalises the last slice
-    const int64_t last_stage = std::max<int64_t>(last_compute, r_hi - 1);
+    const int64_t last_stage = std::max<int64_t>(sp(items - 1) + 3 + (int64_t)d * (W - 1),
+                                                 r_hi > r_lo ? sp(r_hi - 1) : 0);
+    // per stage: receives, then per worker its block (force or pass-through) and the
+    // slices that block completes
     for (int64_t k = 0; k <= last_stage; k++) {
-        if (k >= r_lo && k < r_hi) {
-            const int c = (int)(k % nblk);
-            for (int s = 0; s < blk_count(c); s++)
-                P.ops.push_back({OP_RECV, (int)k, -1, blk_first(c) + s, 1, (int)(k / nblk), -1});
-        }
-        for (int w = 0; w < W; w++) {
-            const int64_t p = k - 2 - (int64_t)d * w;
-            if (p < 0 || p > items) continue;
-            if (p < items) {
-                const int64_t K = p / nblk;
+        for (int64_t p = r_lo; p < r_hi; p++)
+            if (sp(p) == k) {
                 const int c = (int)(p % nblk);
-                if (active(K, w))
-                    P.ops.push_back({OP_FORCE, (int)k, w, blk_first(c), blk_count(c), (int)K,
-                                     K * nw + (int64_t)rank * W + w});
-                else
-                    P.ops.push_back({OP_PASS, (int)k, w, blk_first(c), blk_count(c), (int)K, -1});
+                for (int s = 0; s < blk_count(c); s++)
+                    P.ops.push_back({OP_RECV, (int)k, -1, blk_first(c) + s, 1, (int)(p / nblk), -1});
             }
-            // finalise: last slice of block p-1, then the first count-1 slices of block p
-            auto fin = [&](int64_t K, int first, int cnt) {
+        for (int w = 0; w < W; w++) {
+            // the flat block of worker w at stage k (at most one)
+            int64_t p = -1;
+            {
+                const int64_t q = k - 2 - (int64_t)d * w;   // = sp(p)
+                if (q >= 0) {
+                    const int64_t K = q / ((int64_t)nblk + gap);
+                    const int64_t c = q - K * ((int64_t)nblk + gap);
+                    if (c < nblk) p = K * nblk + c;
+                }
+            }
+            // after the last block: the last slice of the last super-cycle (Table 1's row N_S+3)
+            if (!early_fin && k == sp(items - 1) + 3 + (int64_t)d * w) {
+                const int64_t K = (items - 1) / nblk;
+                if (active(K, w)) P.ops.push_back({OP_BIN, (int)k, w, ns - 1, 1, (int)K, -1});
+                if (w == W - 1) P.ops.push_back({OP_SEND, (int)k, w, ns - 1, 1, (int)K, -1});
+            }
+            if (p < 0 || p >= items) continue;
+            const int64_t K = p / nblk;
+            const int c = (int)(p % nblk);
+            if (active(K, w))
+                P.ops.push_back({OP_FORCE, (int)k, w, blk_first(c), blk_count(c), (int)K,
+                                 K * nw + (int64_t)rank * W + w});
+            else
+                P.ops.push_back({OP_PASS, (int)k, w, blk_first(c), blk_count(c), (int)K, -1});
+            // finalise the slices whose three contributing units are now done: the last
+            // slice of the previous block and all but the last of this block (Table 1);
+            // the last slice of a super-cycle goes with the next super-cycle's first
+            // block -- or, at the plateau, with its own block (x wall: no right
+            // neighbour), so that a super-cycle is complete before the next one starts
+            auto fin = [&](int64_t KK, int first, int cnt) {
                 if (cnt <= 0) return;
-                if (active(K, w)) P.ops.push_back({OP_BIN, (int)k, w, first, cnt, (int)K, -1});
+                if (active(KK, w)) P.ops.push_back({OP_BIN, (int)k, w, first, cnt, (int)KK, -1});
                 if (w == W - 1)
-                    for (int s = 0; s < cnt; s++) P.ops.push_back({OP_SEND, (int)k, w, first + s, 1, (int)K, -1});
+                    for (int s = 0; s < cnt; s++) P.ops.push_back({OP_SEND, (int)k, w, first + s, 1, (int)KK, -1});
             };
-            const bool same_cycle = p >= 1 && p < items && (p % nblk) != 0;
-            if (same_cycle) {
-                const int64_t K = p / nblk;
-                const int c = (int)(p % nblk);
-                fin(K, blk_first(c) - 1, blk_count(c));  // [first-1, first+count-2]
+            if (early_fin) {
+                const int first = c == 0 ? 0 : blk_first(c) - 1;
+                const int last = c == nblk - 1 ? ns - 1 : blk_first(c) + blk_count(c) - 2;
+                fin(K, first, last - first + 1);
+            } else if (c != 0) {
+                fin(K, blk_first(c) - 1, blk_count(c));         // [first-1, first+count-2]
             } else {
-                if (p >= 1) fin((p - 1) / nblk, ns - 1, 1);
-                if (p < items) fin(p / nblk, 0, blk_count(0) - 1);
+                if (p >= 1) fin(K - 1, ns - 1, 1);                // previous super-cycle's last slice
+                fin(K, 0, blk_count(0) - 1);
             }
         }
     }
     P.n_stages = (int)(last_stage + 1);
     return P;
+}
+
+// Idle stages between super-cycles.  With W > 1 workers, worker 0 starts super-cycle
+// K+1 while the later workers still finish K; past Eq. (1)'s bound the
+// data worker 0 waits for from the ring then depends on exactly those trailing
+// blocks, and the stream order would deadlock.  There the ring is at its plateau
+// anyway: a gap of d (W-1) stages lets every rank finish K first.
+bool plan_plateau(int ns, int ng, int W, int B)
+{
+    if (ng == 1) return false;
+    const int nblk = (ns + B - 1) / B;
+    const int d = (B == 1) ? 2 : 1;
+    const char* e = getenv("DSEA_PLAN_GAP");           // sweeps: force on (1) / off (0)
+    if (e && *e) return atoi(e) != 0;
+    // threshold checked against a simulation of all ranks' streams (tests/test_plan_sim.py)
+    return nblk < ng * (3 + d * (W - 1));
+}
+
+int plan_gap(int ns, int ng, int W, int B)
+{
+    const int d = (B == 1) ? 2 : 1;
+    return plan_plateau(ns, ng, W, B) ? d * (W - 1) : 0;
 }
 }  // namespace
 
@@ -1456,6 +1512,26 @@ dsea_status dsea_reset_stats(dsea_ctx* c)
     return DSEA_OK;
 }
 
+dsea_status dsea_plan_ops(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_t W, int64_t n_steps,
+                          int32_t slices_per_stage, int32_t* rows, int64_t cap_rows, int64_t* n_rows)
+{
+    if (!n_rows || n_slices < 1 || n_gpus < 1 || rank < 0 || rank >= n_gpus || W < 1 || n_steps < 0 ||
+        slices_per_stage < 1 || slices_per_stage > n_slices)
+        return DSEA_EINVAL;
+    const Plan P = build_plan(n_slices, n_gpus, rank, W, n_steps, slices_per_stage);
+    *n_rows = (int64_t)P.ops.size();
+    if (!rows) return DSEA_OK;
+    const int64_t n = std::min<int64_t>(cap_rows, (int64_t)P.ops.size());
+    for (int64_t i = 0; i < n; i++) {
+        const Op& op = P.ops[(size_t)i];
+        int32_t* r = rows + 7 * i;
+        r[0] = op.kind; r[1] = op.stage; r[2] = op.worker; r[3] = op.slice; r[4] = op.count;
+        r[5] = op.cycle; r[6] = (int32_t)op.t_rel;
+    }
+    *n_rows = n;
+    return DSEA_OK;
+}
+
 dsea_status dsea_schedule(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_t W, int32_t n_cycles,
                           int32_t* rows, int64_t cap_rows, int64_t* n_rows)
 {
@@ -1481,8 +1557,22 @@ dsea_status dsea_schedule(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_
             r[3] = op.slice + 1; r[6] = op.cycle; r[7] = op.kind == OP_FORCE ? (int32_t)op.t_rel : -1;
             break;
         }
-        case OP_BIN: row_for(st, op.worker)[4] = op.slice + 1; break;
-        case OP_SEND: row_for(st, op.worker)[5] = op.slice + 1; break;
+        // a worker may finalise two runs in one stage (W > 1: the super-cycle's last
+        // slice goes with its own block): the second one gets a row of its own
+        case OP_BIN: {
+            auto* r = &row_for(st, op.worker);
+            if ((*r)[4] >= 0) { out.push_back({st, -1, op.worker, -1, -1, -1, -1, -1}); r = &out.back(); }
+            (*r)[4] = op.slice + 1;
+            break;
+        }
+        case OP_SEND: {
+            std::array<int32_t, 8>* r = nullptr;
+            for (auto& q : out)   // the first row of this (stage, worker) with a free send field
+                if (q[0] == st && q[2] == op.worker && q[5] < 0) { r = &q; break; }
+            if (!r) { out.push_back({st, -1, op.worker, -1, -1, -1, -1, -1}); r = &out.back(); }
+            (*r)[5] = op.slice + 1;
+            break;
+        }
         }
     }
     if (n_gpus == 1) {
@@ -1498,7 +1588,7 @@ dsea_status dsea_schedule(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_
             if (r[1] < 0) { r[1] = j + 1; r[6] = 0; }
         }
     }
-    std::sort(out.begin(), out.end(), [](const std::array<int32_t, 8>& x, const std::array<int32_t, 8>& y) {
+    std::stable_sort(out.begin(), out.end(), [](const std::array<int32_t, 8>& x, const std::array<int32_t, 8>& y) {
         return x[0] != y[0] ? x[0] < y[0] : x[2] < y[2];
     });
     *n_rows = (int64_t)out.size();

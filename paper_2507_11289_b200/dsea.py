@@ -109,6 +109,8 @@ SIGNATURES = [
                                     ctypes.POINTER(dsea_slice_params), ctypes.POINTER(dsea_geometry)]),
     ("dsea_schedule", _st, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                             ctypes.c_int32, _pi32, ctypes.c_int64, _pi64]),
+    ("dsea_plan_ops", _st, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                            ctypes.c_int32, _pi32, ctypes.c_int64, _pi64]),
 ]
 
 
@@ -440,3 +442,17 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+
+OP_RECV, OP_FORCE, OP_PASS, OP_BIN, OP_SEND = range(5)
+
+
+def dsea_plan_ops(n_slices, n_gpus, rank, workers_per_gpu, n_steps, slices_per_stage=1):
+    """Stream-ordered ops of one rank: [n, 7] = kind, stage, worker, slice, count, cycle, t_rel."""
+    n = ctypes.c_int64()
+    _check(None, lib.dsea_plan_ops(n_slices, n_gpus, rank, workers_per_gpu, n_steps, slices_per_stage,
+                                   None, 0, ctypes.byref(n)))
+    rows = np.zeros((n.value, 7), dtype=np.int32)
+    _check(None, lib.dsea_plan_ops(n_slices, n_gpus, rank, workers_per_gpu, n_steps, slices_per_stage,
+                                   rows.ctypes.data_as(_pi32), n.value, ctypes.byref(n)))
+    return rows

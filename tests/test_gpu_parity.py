@@ -152,7 +152,7 @@ def test_cutoff_and_slice_thickness_variants(rc, c_per, ns):
     _cells_exact(e, c)
 
 
-@pytest.mark.parametrize("W,B", [(1, 1), (2, 1), (3, 1), (1, 3), (2, 4), (3, 2)])
+@pytest.mark.parametrize("W,B", [(1, 1), (2, 1), (3, 1), (1, 3), (2, 4), (3, 2), (3, 5)])
 def test_ring_of_one_bitwise_equals_fused(W, B):
     """The stage schedule (Table 1 for B = 1; B slices per stage otherwise; W workers
     sequential on one GPU) and the fused whole-domain pass compute the same
@@ -169,6 +169,23 @@ def test_ring_of_one_bitwise_equals_fused(W, B):
     s2, e2 = e.energies()
     assert s1.tolist() == s2.tolist() == list(range(7))
     assert np.array_equal(e1, e2)
+
+
+@pytest.mark.parametrize("W,B", [(2, 4), (3, 3)])
+def test_ring_of_one_single_slice_last_block(W, B):
+    """13 slices in blocks of B leave a last block of one slice; with W > 1 the next
+    worker's pass on the previous block needs that slice in the same stage, so the
+    plan finalises it with its own block (found by tests/test_plan_sim.py): bitwise
+    equal to the fused pass."""
+    from paper_2507_11289_b200.configs import Config
+    c = Config("r13", 20, 5, 5, 13)
+    ref, _ = _engine(c)
+    ref.step(5)
+    e, _ = _engine(c, workers_per_gpu=W, mode=D.DSEA_MODE_STAGED, slices_per_stage=B)
+    e.step(5)
+    assert np.array_equal(e.positions(), ref.positions())
+    assert np.array_equal(e.velocities(), ref.velocities())
+    assert np.array_equal(e.energies()[1], ref.energies()[1])
 
 
 @pytest.mark.parametrize("maxh,rc", [("24", 2.5), ("40", 2.5), ("", 4.0)])

@@ -57,7 +57,10 @@ CASES = [(2, "P8", 16, 1, 1, 1, "peer"), (2, "P8", 9, 1, 2, 1, "peer"), (2, "P8"
          (2, "P8", 16, 1, 1, 0, "peer"), (2, "P8", 10, 2, 2, 3, "peer"), (2, "P8", 16, 1, 1, 1, "nccl"),
          (2, "P8", 10, 2, 2, 3, "nccl"), (4, "P8", 16, 1, 2, 1, "peer"), (4, "P8", 10, 1, 1, 2, "peer"),
          (4, "P8", 16, 1, 1, 0, "peer"), (4, "P8", 16, 1, 1, 0, "nccl"), (8, "P8", 16, 1, 1, 1, "peer"),
-         (8, "C1", 8, 1, 1, 1, "peer"), (8, "P8", 24, 1, 2, 0, "peer")]
+         (8, "C1", 8, 1, 1, 1, "peer"), (8, "P8", 24, 1, 2, 0, "peer"),
+         # past Eq. (1)'s bound at block level: the ring must run at the plateau, not stall
+         (4, "P8", 10, 2, 1, 3, "peer"), (4, "P8", 12, 3, 1, 2, "peer"), (2, "P8", 11, 3, 1, 4, "peer"),
+         (4, "P8", 12, 2, 1, 3, "nccl")]
 
 
 @pytest.mark.parametrize("n,cfg,steps,workers,calls,block,hop", CASES)

@@ -1,0 +1,80 @@
+"""CPU simulation of the ring's stage plans (dsea_plan_ops, the op lists run_plan
+executes) across all ranks, with the cross-rank data dependencies of the peer
+ring: a worker-0 force/pass of rank r waits until the predecessor's last worker has
+delivered (binned or passed through) every slot it reads for that super-cycle;
+everything else is ordered by the rank's own stream.  Checks, for many (N_S, N_GPU,
+W, B): no deadlock -- in particular beyond Eq. (1)'s N_max, where the ring must run
+at the plateau (Q17) rather than stall -- local inputs binned before use,
+and every (slice, timestep) unit computed exactly once (Q15)."""
+import itertools
+
+import pytest
+
+from paper_2507_11289_b200 import dsea as D
+
+R, F, P, BN, S = D.OP_RECV, D.OP_FORCE, D.OP_PASS, D.OP_BIN, D.OP_SEND
+
+
+def simulate(ns, ng, W, n_steps, B):
+    plans = [D.dsea_plan_ops(ns, ng, r, W, n_steps, B) for r in range(ng)]
+    ptr = [0] * ng
+    # deliveries[r][s]: times slot s of rank r's input buffer was filled by the predecessor
+    deliveries = [[0] * ns for _ in range(ng)]
+    # binned[r][w][s]: times worker w of rank r finalised slot s (its output buffer)
+    binned = [[[0] * ns for _ in range(W)] for _ in range(ng)]
+    done_units = {}
+    progress = True
+    while progress:
+        progress = False
+        for r in range(ng):
+            while ptr[r] < len(plans[r]):
+                kind, stage, w, j, n, K, t = (int(v) for v in plans[r][ptr[r]])
+                if kind in (F, P):
+                    lo = max(j - 1, 0)
+                    hi = min(j + n, ns - 1) if kind == F else j + n - 1
+                    if w == 0:
+                        if ng > 1 and not (r == 0 and K == 0):
+                            need = K + 1 if r > 0 else K
+                            if any(deliveries[r][s] < need for s in range(lo, hi + 1)):
+                                break          # blocked on the ring
+                    else:
+                        # local input: worker w-1's output of this super-cycle, already
+                        # binned earlier in this rank's stream
+                        assert all(binned[r][w - 1][s] >= K + 1 for s in range(lo, hi + 1)), \
+                            ("local order", r, stage, w, j, K)
+                    if kind == F:
+                        for s in range(j, j + n):
+                            key = (s, t)
+                            assert key not in done_units, ("unit twice", key, r)
+                            done_units[key] = r
+                    else:
+                        for s in range(j, j + n):
+                            binned[r][w][s] += 1
+                            if w == W - 1 and ng > 1:
+                                deliveries[(r + 1) % ng][s] += 1
+                elif kind == BN:
+                    for s in range(j, j + n):
+                        binned[r][w][s] += 1
+                        if w == W - 1 and ng > 1:
+                            deliveries[(r + 1) % ng][s] += 1
+                ptr[r] += 1
+                progress = True
+    stuck = [r for r in range(ng) if ptr[r] < len(plans[r])]
+    return stuck, done_units, deliveries
+
+
+CASES = [(ns, ng, W, B) for ns, ng, W, B in itertools.product(
+    (6, 8, 12, 13, 16, 24, 32, 48, 64), (2, 3, 4, 8), (1, 2, 3), (1, 2, 3, 4, 8))
+    if B <= ns and ns >= 2 + 2 * W]
+
+
+@pytest.mark.parametrize("ns,ng,W,B", CASES)
+def test_ring_plan_completes_and_covers_every_unit(ns, ng, W, B):
+    cycles = 3
+    n_steps = cycles * ng * W - (W > 1)      # not a multiple of N_w: pass-through (Q15)
+    stuck, units, deliveries = simulate(ns, ng, W, n_steps, B)
+    assert not stuck, f"deadlock: ranks {stuck} blocked (ns={ns} ng={ng} W={W} B={B})"
+    assert len(units) == ns * n_steps
+    assert set(units) == {(s, t) for s in range(ns) for t in range(n_steps)}
+    # the state returns to rank 0 after the last super-cycle (Q22)
+    assert all(d == cycles for d in deliveries[0])
