@@ -140,29 +140,63 @@ struct Plan {
     int n_stages = 0;
 };
 
-bool plan_plateau(int ns, int ng, int W, int B);
-int plan_gap(int ns, int ng, int W, int B);
+// Partition of the N_S slices into the blocks of a super-cycle: uniform blocks of B
+// slices (the last one may be shorter).  Optional (DSEA_LEAD_BLOCKS=1, ring, B >= 4):
+// the first two blocks have 2 slices ("lead" blocks), so rank g+1 can start a
+// super-cycle after rank g processed 4 slices instead of 2 B (a one-slice tail is
+// merged into its predecessor, so every block has >= 2 slices and d stays 1).
+// Measured on 4 B200s (C4, B = 7): 0.9 % slower -- the steady-state lag between
+// ranks is two blocks of the current size, so the earlier start only turns into a
+// stall at the first full-size block and the drain keeps the full lag.
+struct Blocks {
+    std::vector<int> first;   // nblk + 1 entries, first[nblk] = ns
+    std::vector<int> of;      // block of each slice
+    int d = 1;                // worker w+1 trails worker w by d stages
+    int n() const { return (int)first.size() - 1; }
+    int count(int c) const { return first[c + 1] - first[c]; }
+};
 
-Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps, int B)
+Blocks make_blocks(int ns, int ng, int B)
+{
+    Blocks bl;
+    if (B < 1) B = 1;
+    const char* e = getenv("DSEA_LEAD_BLOCKS");          // sweeps: 0 disables the lead blocks
+    const bool lead = ng > 1 && B >= 4 && ns >= 4 + 2 * B && e && *e && atoi(e) != 0;
+    int f = 0;
+    if (lead)
+        for (int k = 0; k < 2; k++) { bl.first.push_back(f); f += 2; }
+    while (f < ns) { bl.first.push_back(f); f += B; }
+    if (lead && bl.first.size() > 1 && ns - bl.first.back() == 1) bl.first.pop_back();
+    bl.first.push_back(ns);
+    bl.of.assign(ns, 0);
+    for (int c = 0; c < bl.n(); c++)
+        for (int s = bl.first[c]; s < bl.first[c + 1]; s++) bl.of[s] = c;
+    bl.d = (B == 1) ? 2 : 1;
+    return bl;
+}
+
+bool plan_plateau(int ng, int W, const Blocks& bl);
+int plan_gap(int ng, int W, const Blocks& bl);
+
+Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps, const Blocks& bl)
 {
     Plan P;
-    if (B < 1) B = 1;
-    const int nblk = (ns + B - 1) / B;
-    const int d = (B == 1) ? 2 : 1;
+    const int nblk = bl.n();
+    const int d = bl.d;
     // past Eq. (1)'s bound: close each super-cycle before the next (see plan_gap).
     // With W > 1 the last slice is always finalised with its own block: worker w+1
     // processes the previous block in the same stage and, when the last block is a
     // single slice, needs it (found by tests/test_plan_sim.py).
-    const bool plateau = plan_plateau(ns, ng, W, B);
+    const bool plateau = plan_plateau(ng, W, bl);
     const bool early_fin = plateau || W > 1;
-    const int gap = plan_gap(ns, ng, W, B);
+    const int gap = plan_gap(ng, W, bl);
     const int64_t nw = (int64_t)ng * W;
     const int64_t n_cycles = n_steps <= 0 ? 0 : (n_steps + nw - 1) / nw;
     const int64_t items = n_cycles * nblk;
     if (items == 0) return P;
     auto active = [&](int64_t K, int w) { return K * nw + (int64_t)rank * W + w < n_steps; };
-    auto blk_first = [&](int c) { return c * B; };
-    auto blk_count = [&](int c) { return std::min(B, ns - c * B); };
+    auto blk_first = [&](int c) { return bl.first[c]; };
+    auto blk_count = [&](int c) { return bl.count(c); };
     // stage of flat block p: receive at sp(p), worker w processes it at sp(p) + 2 + d*w,
     // where sp(p) = p + gap * (p / nblk) (gap idle stages after each super-cycle)
     auto sp = [&](int64_t p) { return p + (int64_t)gap * (p / nblk); };
@@ -239,21 +273,20 @@ Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps, int B)
 // data worker 0 waits for from the ring then depends on exactly those trailing
 // blocks, and the stream order would deadlock.  There the ring is at its plateau
 // anyway: a gap of d (W-1) stages lets every rank finish K first.
-bool plan_plateau(int ns, int ng, int W, int B)
+bool plan_plateau(int ng, int W, const Blocks& bl)
 {
     if (ng == 1) return false;
-    const int nblk = (ns + B - 1) / B;
-    const int d = (B == 1) ? 2 : 1;
+    const int nblk = bl.n();
+    const int d = bl.d;
     const char* e = getenv("DSEA_PLAN_GAP");           // sweeps: force on (1) / off (0)
     if (e && *e) return atoi(e) != 0;
     // threshold checked against a simulation of all ranks' streams (tests/test_plan_sim.py)
     return nblk < ng * (3 + d * (W - 1));
 }
 
-int plan_gap(int ns, int ng, int W, int B)
+int plan_gap(int ng, int W, const Blocks& bl)
 {
-    const int d = (B == 1) ? 2 : 1;
-    return plan_plateau(ns, ng, W, B) ? d * (W - 1) : 0;
+    return plan_plateau(ng, W, bl) ? bl.d * (W - 1) : 0;
 }
 }  // namespace
 
@@ -274,6 +307,7 @@ struct dsea_ctx {
     SlotLayout L{};
     int mode = DSEA_MODE_FUSED;
     int W = 1, NG = 1, rank = 0, device = 0, B = 1;
+    Blocks bl;                            // block partition of a super-cycle (make_blocks)
 
     cudaStream_t cs = nullptr, ss = nullptr, rs = nullptr, es = nullptr, bs = nullptr;  // compute, send, recv, energy, remote bin
     BufView inb{};
@@ -685,7 +719,7 @@ enum { TK_FORCE = 0, TK_BIN = 1, TK_SEND = 2 };
 dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
 {
     const int ns = c->g.ns;
-    const Plan P = build_plan(ns, c->NG, c->rank, c->W, n_steps, c->B);
+    const Plan P = build_plan(ns, c->NG, c->rank, c->W, n_steps, c->bl);
     std::vector<char> sent(ns, 0);
     const size_t sb = c->L.slot_bytes;
     NcclApi& api = nccl();
@@ -733,14 +767,12 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             // this block's per-atom energy records of the previous super-cycle must be
             // reduced before the pass rewrites them (other blocks' reductions may still
             // run: they overlap this pass instead of stalling it)
-            const int nblk_e = (ns + c->B - 1) / c->B;
-            cudaEvent_t& ev_e = c->ev_energy[(size_t)w * nblk_e + (j / c->B) % nblk_e];
+            cudaEvent_t& ev_e = c->ev_energy[(size_t)w * c->bl.n() + c->bl.of[j]];
             if (c->T.pipe) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, ev_e, 0));
             if (c->peer && !c->ce_hop && w == W - 1) {
                 // staging of this block and the arrival counters it adds to were last read
                 // by the remote bin runs of blocks c and c+1 one super-cycle ago
-                const int nblk = (ns + c->B - 1) / c->B;
-                CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_binblk[(j / c->B + 1) % nblk], 0));
+                CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_binblk[(c->bl.of[j] + 1) % c->bl.n()], 0));
             }
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
             c->stats.kernel_launches +=
@@ -827,9 +859,9 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 // then the copy stream pushes the finished slots over NVLink and raises
                 // the successor's arrival flags -- neither needs an SM, so both overlap
                 // the next block's (persistent, SM-filling) force pass
-                const int nblk = (ns + c->B - 1) / c->B;
-                for (int k = m / c->B; k <= (m + n - 1) / c->B; k++)   // previous push of these slots
-                    if (c->hop_rec[k % nblk]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_hop[k % nblk], 0));
+                const int nblk = c->bl.n();
+                for (int k = c->bl.of[m]; k <= c->bl.of[m + n - 1]; k++)   // previous push of these slots
+                    if (c->hop_rec[k]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_hop[k], 0));
                 cudaEvent_t t0 = nullptr, t1 = nullptr;
                 if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
                 const int s0 = std::max(m - 1, 0), s1 = std::min(m + n, ns - 1);
@@ -854,7 +886,7 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                     if (write_value32()(c->bs, (unsigned long long)(c->succ_arr + sl), wv, 0))
                         return fail(c, DSEA_EPEER, "cuStreamWriteValue32 (arrival) failed");
                 if (c->timing) { cudaEventRecord(h1, c->bs); c->tpairs.push_back({TK_SEND, {h0, h1}}); }
-                const int key = ((m + n - 1) / c->B) % nblk;
+                const int key = c->bl.of[m + n - 1] % nblk;
                 CUDA_TRY(c, cudaEventRecord(c->ev_hop[key], c->bs));
                 c->hop_rec[key] = 1;
                 c->stats.hop_bytes += (int64_t)sb * n;
@@ -897,8 +929,7 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                     c->stats.hop_bytes += (int64_t)sb * n;
                     // keyed by the block of this run's last slot: a force pass on block c
                     // waits for the run covering slot (c+1)B, i.e. key c+1
-                    const int nblk = (ns + c->B - 1) / c->B;
-                    CUDA_TRY(c, cudaEventRecord(c->ev_binblk[((m + n - 1) / c->B) % nblk], bst));
+                    CUDA_TRY(c, cudaEventRecord(c->ev_binblk[c->bl.of[m + n - 1]], bst));
                 } else {
                     for (int sl = m; sl < m + n; sl++) CUDA_TRY(c, cudaEventRecord(c->ev_bin[sl], c->cs));
                 }
@@ -1079,6 +1110,7 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     c->W = sp->workers_per_gpu;
     c->B = B;
     c->NG = sp->n_gpus;
+    c->bl = make_blocks(geo.n_slices, c->NG, B);
     c->rank = sp->rank;
     c->device = sp->device;
 
@@ -1154,7 +1186,7 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     c->T.ctr_base = &c->tile_ctr_base;
     CUDA_TRY(c, cudaMemset(c->err_dev, 0, sizeof(DevErr)));
     {
-        const int nblk = (g.ns + c->B - 1) / c->B;
+        const int nblk = c->bl.n();
         c->ev_binblk.resize(nblk);
         for (int k = 0; k < nblk; k++) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_binblk[k], cudaEventDisableTiming));
         c->ev_hop.resize(nblk);
@@ -1163,7 +1195,7 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     }
     c->ev_force.resize(c->W);
     for (int w = 0; w < c->W; w++) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_force[w], cudaEventDisableTiming));
-    c->ev_energy.resize((size_t)c->W * ((g.ns + c->B - 1) / c->B));
+    c->ev_energy.resize((size_t)c->W * c->bl.n());
     for (auto& e : c->ev_energy) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto* v : {&c->ev_recv, &c->ev_free, &c->ev_bin, &c->ev_send}) {
         v->resize(g.ns);
@@ -1518,7 +1550,7 @@ dsea_status dsea_plan_ops(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_
     if (!n_rows || n_slices < 1 || n_gpus < 1 || rank < 0 || rank >= n_gpus || W < 1 || n_steps < 0 ||
         slices_per_stage < 1 || slices_per_stage > n_slices)
         return DSEA_EINVAL;
-    const Plan P = build_plan(n_slices, n_gpus, rank, W, n_steps, slices_per_stage);
+    const Plan P = build_plan(n_slices, n_gpus, rank, W, n_steps, make_blocks(n_slices, n_gpus, slices_per_stage));
     *n_rows = (int64_t)P.ops.size();
     if (!rows) return DSEA_OK;
     const int64_t n = std::min<int64_t>(cap_rows, (int64_t)P.ops.size());
@@ -1538,7 +1570,7 @@ dsea_status dsea_schedule(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_
     if (!n_rows || n_slices < 1 || n_gpus < 1 || rank < 0 || rank >= n_gpus || W < 1 || n_cycles < 0)
         return DSEA_EINVAL;
     const int64_t n_steps = (int64_t)n_cycles * n_gpus * W;
-    const Plan P = build_plan(n_slices, n_gpus, rank, W, n_steps, 1);
+    const Plan P = build_plan(n_slices, n_gpus, rank, W, n_steps, make_blocks(n_slices, n_gpus, 1));
     // one row per (stage, worker) doing something; recv rows carry worker -1
     std::vector<std::array<int32_t, 8>> out;
     auto row_for = [&](int stage, int worker) -> std::array<int32_t, 8>& {

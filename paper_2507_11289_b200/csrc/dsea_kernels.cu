@@ -28,6 +28,14 @@ namespace dsea {
 
 #define FULLMASK 0xffffffffu
 
+// Programmatic dependent launch (PDL): kernels of the compute-stream chain (force ->
+// bin scan -> place -> gather -> next force) are launched with programmatic stream
+// serialisation, so a launch and its CTAs' prologue overlap the predecessor's tail.
+// pdl_wait() blocks until the predecessor grid has completed and its memory is
+// visible (a no-op without PDL); pdl_release() lets the successor launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void set_err(DevErr* e, int code, int slice, int atom, int aux) {
     if (atomicCAS(&e->code, 0, code) == 0) {
         e->slice = slice;
@@ -611,6 +619,8 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
              DevErr* __restrict__ err, unsigned long long* __restrict__ tile_ctr,
              unsigned long long ctr_base)
 {
+    pdl_wait();
+    pdl_release();
     constexpr int IL = 32 / JPAR;           // atoms per chunk; JPAR lanes per atom
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ PipeMeta meta[2];
@@ -990,6 +1000,8 @@ constexpr int ENERGY_THREADS = 256;
 __global__ void __launch_bounds__(ENERGY_THREADS)
 k_energy(Geo g, StgView stg, int j0, UnitEnergy* __restrict__ e_out)
 {
+    pdl_wait();
+    pdl_release();
     const int j = j0 + blockIdx.x;
     const int n = stg.n[j];
     const double4* e = stg.eatom + (size_t)j * g.cap;
@@ -1032,6 +1044,8 @@ __global__ void __launch_bounds__(DRIFT_THREADS)
 k_drift(Geo g, StgView stg, int j0, const UnitEnergy* __restrict__ e_out, int32_t* __restrict__ out_cnt,
         DevErr* __restrict__ err)
 {
+    pdl_wait();
+    pdl_release();
     const int j = j0 + blockIdx.y;
     const int n = stg.n[j];
     const double lam = e_out[j].lambda;
@@ -1056,6 +1070,8 @@ constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_ITEMS;
 __global__ void __launch_bounds__(SCAN_THREADS)
 k_bin_scan(Geo g, BufView out, int m0, DevErr* err)
 {
+    pdl_wait();
+    pdl_release();
     __shared__ int buf[SCAN_CHUNK];
     __shared__ int wsum[32];
     __shared__ int carry_s;
@@ -1120,6 +1136,8 @@ constexpr int PLACE_THREADS = 256;
 __global__ void __launch_bounds__(PLACE_THREADS)
 k_bin_place(Geo g, BufView out, StgView stg, int s0, int flat_count, int m0, int nm)
 {
+    pdl_wait();
+    pdl_release();
     int base, n;
     if (flat_count > 0) { base = 0; n = flat_count; }
     else { const int s = s0 + blockIdx.y; base = s * g.cap; n = stg.n[s]; }
@@ -1157,6 +1175,8 @@ template <int CM>
 __global__ void __launch_bounds__(GATHER_THREADS)
 k_bin_gather(Geo g, BufView out, StgView stg, int m0)
 {
+    pdl_wait();
+    pdl_release();
     __shared__ double kz[GATHER_CELLS][CM + 1];
     __shared__ int kid[GATHER_CELLS][CM + 1];
     __shared__ int ksrc[GATHER_CELLS][CM + 1];
@@ -1309,6 +1329,28 @@ static double env_num(const char* name, double dflt)
     return (v && *v) ? atof(v) : dflt;
 }
 
+// launch with programmatic stream serialisation (DSEA_PDL=0: plain launches, A/B)
+static bool pdl_on()
+{
+    static const bool on = env_num("DSEA_PDL", 1) != 0;
+    return on;
+}
+template <typename... KArgs, typename... Args>
+static void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
 {
     // defaults from the B200 measurements in profiles/; DSEA_* overrides for sweeps
@@ -1383,11 +1425,11 @@ int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t
         // NVE: force + kick + drift + destination in one pass; NVT: force + kick (the
         // drift needs the slice's lambda, k_drift)
         if (g.thermo)
-            k_force_pipe<2, true><<<T.grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err,
-                                                                       T.ctr, *T.ctr_base);
+            launch(k_force_pipe<2, true>, T.grid, PIPE_THREADS, T.smem, s, g, T, in, stg, out_cnt, j0, nj, err,
+                   T.ctr, *T.ctr_base);
         else
-            k_force_pipe<2, false><<<T.grid, PIPE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, nj, err,
-                                                                        T.ctr, *T.ctr_base);
+            launch(k_force_pipe<2, false>, T.grid, PIPE_THREADS, T.smem, s, g, T, in, stg, out_cnt, j0, nj, err,
+                   T.ctr, *T.ctr_base);
         *T.ctr_base += (unsigned long long)nj * T.tiles + T.grid;
         return 1;
     }
@@ -1406,6 +1448,8 @@ int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t
 // count in the successor's flag array (or a release count in the predecessor's).
 __global__ void k_signal(uint32_t* __restrict__ flags, int first, int n, uint32_t value)
 {
+    pdl_wait();
+    pdl_release();
     __threadfence_system();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         volatile uint32_t* f = flags + first + i;
@@ -1416,24 +1460,24 @@ __global__ void k_signal(uint32_t* __restrict__ flags, int first, int n, uint32_
 
 void signal_launch(uint32_t* flags, int first, int n, uint32_t value, cudaStream_t s)
 {
-    k_signal<<<1, 64, 0, s>>>(flags, first, n, value);
+    launch(k_signal, 1, 64, 0, s, flags, first, n, value);
 }
 
 void energy_launch(const Geo& g, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s)
 {
-    k_energy<<<nj, ENERGY_THREADS, 0, s>>>(g, stg, j0, e_out);
+    launch(k_energy, nj, ENERGY_THREADS, 0, s, g, stg, j0, e_out);
 }
 
 void drift_launch(const Geo& g, StgView stg, int j0, int nj, const UnitEnergy* e_out, int32_t* out_cnt,
                   DevErr* err, cudaStream_t s)
 {
     dim3 grid((unsigned)std::max(1, std::min((g.cap + DRIFT_THREADS - 1) / DRIFT_THREADS, 64)), (unsigned)nj);
-    k_drift<<<grid, DRIFT_THREADS, 0, s>>>(g, stg, j0, e_out, out_cnt, err);
+    launch(k_drift, grid, DRIFT_THREADS, 0, s, g, stg, j0, e_out, out_cnt, err);
 }
 
 void bin_scan_launch(const Geo& g, BufView out, int m0, int nm, DevErr* err, cudaStream_t s)
 {
-    k_bin_scan<<<nm, SCAN_THREADS, 0, s>>>(g, out, m0, err);
+    launch(k_bin_scan, nm, SCAN_THREADS, 0, s, g, out, m0, err);
 }
 
 void bin_place_launch(const Geo& g, BufView out, StgView stg, int s0, int nsrc, int flat_count,
@@ -1442,10 +1486,10 @@ void bin_place_launch(const Geo& g, BufView out, StgView stg, int s0, int nsrc, 
     (void)err;
     if (flat_count > 0) {
         dim3 grid((flat_count + PLACE_THREADS - 1) / PLACE_THREADS, 1);
-        k_bin_place<<<grid, PLACE_THREADS, 0, s>>>(g, out, stg, 0, flat_count, m0, nm);
+        launch(k_bin_place, grid, PLACE_THREADS, 0, s, g, out, stg, 0, flat_count, m0, nm);
     } else {
         dim3 grid((g.cap + PLACE_THREADS - 1) / PLACE_THREADS, nsrc);
-        k_bin_place<<<grid, PLACE_THREADS, 0, s>>>(g, out, stg, s0, 0, m0, nm);
+        launch(k_bin_place, grid, PLACE_THREADS, 0, s, g, out, stg, s0, 0, m0, nm);
     }
 }
 
@@ -1454,9 +1498,9 @@ void bin_gather_launch(const Geo& g, BufView out, StgView stg, int m0, int nm, D
 {
     (void)err;
     dim3 grid((g.ncell + GATHER_CELLS - 1) / GATHER_CELLS, nm);
-    if (g.cell_max <= 32) k_bin_gather<32><<<grid, GATHER_THREADS, 0, s>>>(g, out, stg, m0);
-    else if (g.cell_max <= 64) k_bin_gather<64><<<grid, GATHER_THREADS, 0, s>>>(g, out, stg, m0);
-    else k_bin_gather<128><<<grid, GATHER_THREADS, 0, s>>>(g, out, stg, m0);
+    if (g.cell_max <= 32) launch(k_bin_gather<32>, grid, GATHER_THREADS, 0, s, g, out, stg, m0);
+    else if (g.cell_max <= 64) launch(k_bin_gather<64>, grid, GATHER_THREADS, 0, s, g, out, stg, m0);
+    else launch(k_bin_gather<128>, grid, GATHER_THREADS, 0, s, g, out, stg, m0);
 }
 
 void init_keys_launch(const Geo& g, StgView stg, int n, int32_t* out_cnt, DevErr* err,

@@ -258,6 +258,39 @@ def test_full_size_c2_sampled_forces_and_cells():
     _cells_exact(e, c)
 
 
+def test_full_size_c4_bench_workload():
+    """C4 -- the bench workload (16,384,000 atoms, 109 slices, paper slicing rule) -- in
+    the launch configuration bench.py times (fused, one GPU): forces on 256 sampled
+    atoms against the oracle's all-pairs sums (Q13), every atom's cell and slice
+    bit-exact (Q4), and over 10 further steps the properties that hold at any size:
+    atom count, zero net force (the walls exert none, Alg. 1 pairs cancel) and
+    conserved y/z momentum (the walls only flip v_x, Q1/Q2)."""
+    e, c = _engine("C4")
+    g = _geom(c)
+    x = inputs.jitter(oracle.lattice(c.nx, c.ny, c.nz, g.a), g.b, 0.2, 9)
+    v = inputs.gaussian_velocities(c.n_atoms, 1.0, 9)
+    e.set_state(x, v)
+    e.step(1)
+    rng = np.random.default_rng(1)
+    idx = np.sort(rng.choice(c.n_atoms, 256, replace=False))
+    Fo, _ = oracle.forces_subset(x, g.b, c.rc, idx)
+    F = e.forces()
+    frms_o = np.sqrt((Fo ** 2).sum(1).mean())
+    err = np.sqrt(((F[idx] - Fo) ** 2).sum(1)) / np.maximum(np.sqrt((Fo ** 2).sum(1)), frms_o)
+    assert err.max() <= 1e-10, err.max()
+    _cells_exact(e, c)
+    p0 = e.velocities().sum(0)
+    e.step(10)
+    F = e.forces()
+    frms = np.sqrt((F ** 2).sum(1).mean())
+    assert np.abs(F.sum(0)).max() <= 1e-12 * c.n_atoms * frms
+    v1 = e.velocities()
+    assert v1.shape[0] == c.n_atoms
+    assert np.abs(v1.sum(0)[1:] - p0[1:]).max() <= 1e-10 * np.abs(v1).sum(0)[1:].max()
+    _cells_exact(e, c)
+    e.close()
+
+
 def test_error_paths():
     e, c = _engine("C1")
     g = _geom(c)

@@ -40,14 +40,15 @@ def _single(cfg, steps, thermo=0.0):
     return r
 
 
-def _ring(tmp_path, n, cfg, steps, workers=1, calls=1, block=0, hop="peer", thermo=0.0):
+def _ring(tmp_path, n, cfg, steps, workers=1, calls=1, block=0, hop="peer", thermo=0.0, env=None):
     out = str(tmp_path / f"ring_{n}_{cfg}_{steps}_{workers}_{calls}_{block}_{hop}_{thermo}.npz")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={29500 + n * 7 + steps}",
            os.path.join(ROOT, "tests", "ring_worker.py"), "--config", cfg, "--steps", str(steps),
            "--workers", str(workers), "--calls", str(calls), "--block", str(block), "--hop", hop,
            "--thermo", str(thermo), "--out", out]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env=None if env is None else {**os.environ, **env})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return np.load(out)
 
@@ -60,18 +61,24 @@ CASES = [(2, "P8", 16, 1, 1, 1, "peer"), (2, "P8", 9, 1, 2, 1, "peer"), (2, "P8"
          (8, "C1", 8, 1, 1, 1, "peer"), (8, "P8", 24, 1, 2, 0, "peer"),
          # past Eq. (1)'s bound at block level: the ring must run at the plateau, not stall
          (4, "P8", 10, 2, 1, 3, "peer"), (4, "P8", 12, 3, 1, 2, "peer"), (2, "P8", 11, 3, 1, 4, "peer"),
-         (4, "P8", 12, 2, 1, 3, "nccl")]
+         (4, "P8", 12, 2, 1, 3, "nccl"),
+         # full size: C3 (2,048,000 atoms, 256 slices) with the bench's automatic block size
+         (2, "C3", 4, 1, 1, 0, "peer"), (4, "C3", 8, 1, 1, 0, "peer")]
+# optional lead blocks (DSEA_LEAD_BLOCKS=1: 2 + 2 slices, then B): both backends, W = 2, several calls
+LEAD_CASES = [(2, "P8", 12, 2, 1, 5, "peer"), (4, "P8", 12, 1, 1, 5, "nccl"), (2, "P8", 12, 1, 2, 6, "nccl"),
+              (4, "P8", 16, 1, 2, 4, "peer")]
 
 
-@pytest.mark.parametrize("n,cfg,steps,workers,calls,block,hop", CASES)
-def test_ring_bitwise_equals_single_gpu(tmp_path, n, cfg, steps, workers, calls, block, hop):
+@pytest.mark.parametrize("n,cfg,steps,workers,calls,block,hop,lead",
+                         [c + (False,) for c in CASES] + [c + (True,) for c in LEAD_CASES])
+def test_ring_bitwise_equals_single_gpu(tmp_path, n, cfg, steps, workers, calls, block, hop, lead):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
     c = CONFIGS[cfg]
     if c.n_slices < 2 + 2 * workers:
         pytest.skip("too few slices")
     x, v, f, s1, e1, _ = _single(cfg, steps)
-    r = _ring(tmp_path, n, cfg, steps, workers, calls, block, hop)
+    r = _ring(tmp_path, n, cfg, steps, workers, calls, block, hop, env={"DSEA_LEAD_BLOCKS": "1"} if lead else None)
     assert np.array_equal(r["x"], x)
     assert np.array_equal(r["v"], v)
     assert np.array_equal(r["f"], f)

@@ -78,3 +78,36 @@ def test_ring_plan_completes_and_covers_every_unit(ns, ng, W, B):
     assert set(units) == {(s, t) for s in range(ns) for t in range(n_steps)}
     # the state returns to rank 0 after the last super-cycle (Q22)
     assert all(d == cycles for d in deliveries[0])
+
+
+# the benchmark's ring configurations (C4: 109 slices, auto B = 7 at 2/4 GPUs, 4 at 8;
+# C3: 256 slices) including the lead blocks of make_blocks
+BENCH_CASES = [(109, 2, 1, 7), (109, 4, 1, 7), (109, 8, 1, 4), (109, 4, 2, 5), (256, 8, 1, 7), (20, 2, 1, 6)]
+
+
+@pytest.mark.parametrize("lead", ["0", "1"])
+@pytest.mark.parametrize("ns,ng,W,B", BENCH_CASES)
+def test_bench_ring_plans(ns, ng, W, B, lead, monkeypatch):
+    monkeypatch.setenv("DSEA_LEAD_BLOCKS", lead)
+    n_steps = 2 * ng * W
+    stuck, units, deliveries = simulate(ns, ng, W, n_steps, B)
+    assert not stuck
+    assert set(units) == {(s, t) for s in range(ns) for t in range(n_steps)}
+    assert all(d == 2 for d in deliveries[0])
+
+
+@pytest.mark.parametrize("ns,ng,B,lead", [(109, 4, 7, True), (109, 8, 4, True), (109, 1, 7, False),
+                                          (109, 4, 3, False), (11, 2, 4, False), (20, 2, 6, True)])
+def test_lead_blocks(ns, ng, B, lead, monkeypatch):
+    """On a ring the first two blocks of a super-cycle hold 2 slices (shorter per-rank
+    pipeline lag), the rest B; every block has >= 2 slices then; uniform otherwise."""
+    monkeypatch.setenv("DSEA_LEAD_BLOCKS", "1")
+    ops = D.dsea_plan_ops(ns, ng, 0, 1, ng, B)
+    sizes = [int(o[4]) for o in ops if int(o[0]) in (F, P) and int(o[5]) == 0]
+    assert sum(sizes) == ns
+    if lead:
+        assert sizes[:2] == [2, 2]
+        assert all(sz >= 2 for sz in sizes)
+        assert all(sz in (B, B + 1) for sz in sizes[2:-1])
+    else:
+        assert sizes[:-1] == [B] * (len(sizes) - 1)
