@@ -140,14 +140,14 @@ struct Plan {
     int n_stages = 0;
 };
 
-// Partition of the N_S slices into the blocks of a super-cycle: uniform blocks of B
-// slices (the last one may be shorter).  Optional (DSEA_LEAD_BLOCKS=1, ring, B >= 4):
-// the first two blocks have 2 slices ("lead" blocks), so rank g+1 can start a
-// super-cycle after rank g processed 4 slices instead of 2 B (a one-slice tail is
-// merged into its predecessor, so every block has >= 2 slices and d stays 1).
-// Measured on 4 B200s (C4, B = 7): 0.9 % slower -- the steady-state lag between
-// ranks is two blocks of the current size, so the earlier start only turns into a
-// stall at the first full-size block and the drain keeps the full lag.
+// Partition of the N_S slices into the blocks of a super-cycle: nblk = ceil(N_S / B)
+// blocks of balanced size (sizes differ by at most one slice, so no short tail block:
+// a one-slice tail block cost up to 4 % on the C4 ring, profiles/r01/ring_tuning).
+// Optional (DSEA_LEAD_BLOCKS=1, ring, B >= 4): the first two blocks have 2 slices
+// ("lead" blocks), so rank g+1 can start a super-cycle after rank g processed 4 slices
+// instead of 2 B.  Measured on 4 B200s (C4, B = 7): 0.9 % slower -- the steady-state
+// lag between ranks is two blocks of the current size, so the earlier start only turns
+// into a stall at the first full-size block and the drain keeps the full lag.
 struct Blocks {
     std::vector<int> first;   // nblk + 1 entries, first[nblk] = ns
     std::vector<int> of;      // block of each slice
@@ -160,13 +160,14 @@ Blocks make_blocks(int ns, int ng, int B)
 {
     Blocks bl;
     if (B < 1) B = 1;
-    const char* e = getenv("DSEA_LEAD_BLOCKS");          // sweeps: 0 disables the lead blocks
+    const char* e = getenv("DSEA_LEAD_BLOCKS");
     const bool lead = ng > 1 && B >= 4 && ns >= 4 + 2 * B && e && *e && atoi(e) != 0;
     int f = 0;
     if (lead)
         for (int k = 0; k < 2; k++) { bl.first.push_back(f); f += 2; }
-    while (f < ns) { bl.first.push_back(f); f += B; }
-    if (lead && bl.first.size() > 1 && ns - bl.first.back() == 1) bl.first.pop_back();
+    const int rest = ns - f;
+    const int nb = (rest + B - 1) / B;
+    for (int k = 0; k < nb; k++) bl.first.push_back(f + (int)((int64_t)rest * k / nb));
     bl.first.push_back(ns);
     bl.of.assign(ns, 0);
     for (int c = 0; c < bl.n(); c++)
@@ -1077,9 +1078,14 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     int B = sp->slices_per_stage;
     if (B < 0) return fail(c, DSEA_EINVAL, "slices_per_stage < 0");
     if (B == 0) {
-        const double per_slice = (double)geo.n_atoms / geo.n_slices;
-        B = std::max(1, (int)std::ceil(1.0e6 / per_slice));
-        const int depth = sp->n_gpus * (2 + sp->workers_per_gpu);
+        // ~2e6 atoms per launch, but >= N_GPU (2 + W) - 1 blocks per super-cycle so the
+        // ring stays busy (each rank trails its predecessor by two blocks; Eq. (1));
+        // tuned on 2 and 4 B200s (profiles/r01/ring_tuning: C4 best at 8-9 blocks on 2
+        // GPUs, 11 on 4)
+        const int nb_t = (int)std::ceil((double)geo.n_atoms / 2.0e6);
+        const int depth = sp->n_gpus > 1 ? sp->n_gpus * (2 + sp->workers_per_gpu) - 1 : 2 + sp->workers_per_gpu;
+        const int nb = std::max(1, std::max(nb_t, depth));
+        B = std::max(1, (geo.n_slices + nb - 1) / nb);
         while (B > 1 && (geo.n_slices + B - 1) / B < depth) B--;
         if (mode == DSEA_MODE_FUSED) B = 1;
     }

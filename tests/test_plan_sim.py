@@ -99,15 +99,16 @@ def test_bench_ring_plans(ns, ng, W, B, lead, monkeypatch):
 @pytest.mark.parametrize("ns,ng,B,lead", [(109, 4, 7, True), (109, 8, 4, True), (109, 1, 7, False),
                                           (109, 4, 3, False), (11, 2, 4, False), (20, 2, 6, True)])
 def test_lead_blocks(ns, ng, B, lead, monkeypatch):
-    """On a ring the first two blocks of a super-cycle hold 2 slices (shorter per-rank
-    pipeline lag), the rest B; every block has >= 2 slices then; uniform otherwise."""
+    """Blocks are balanced (ceil(N_S / B) blocks whose sizes differ by at most one, so
+    no short tail block); with DSEA_LEAD_BLOCKS=1 on a ring the first two blocks of a
+    super-cycle hold 2 slices (shorter per-rank pipeline lag), the rest balanced."""
     monkeypatch.setenv("DSEA_LEAD_BLOCKS", "1")
     ops = D.dsea_plan_ops(ns, ng, 0, 1, ng, B)
     sizes = [int(o[4]) for o in ops if int(o[0]) in (F, P) and int(o[5]) == 0]
     assert sum(sizes) == ns
+    rest = sizes[2:] if lead else sizes
     if lead:
         assert sizes[:2] == [2, 2]
-        assert all(sz >= 2 for sz in sizes)
-        assert all(sz in (B, B + 1) for sz in sizes[2:-1])
-    else:
-        assert sizes[:-1] == [B] * (len(sizes) - 1)
+    assert len(rest) == -(-(ns - (4 if lead else 0)) // B)
+    assert max(rest) <= B and max(rest) - min(rest) <= 1
+    assert all(sz >= 2 for sz in sizes)
