@@ -51,3 +51,20 @@ def jitter(xyz: np.ndarray, box, amp: float, seed: int) -> np.ndarray:
 def gaussian_velocities(n: int, scale: float, seed: int) -> np.ndarray:
     rng = np.random.default_rng(seed)
     return rng.standard_normal((n, 3)) * scale
+
+
+def grid_field(nx: int, ny: int, nz: int, seed: int) -> np.ndarray:
+    """Seeded synthetic scalar field for the stencil workload: a
+    smooth part (a few random low Fourier modes, like a large-scale temperature or
+    velocity component) plus uniform noise, shape (nx, ny, nz), float64."""
+    rng = np.random.default_rng(seed)
+    x = (np.arange(nx) + 0.5)[:, None, None] / nx
+    y = np.arange(ny)[None, :, None] / ny
+    z = np.arange(nz)[None, None, :] / nz
+    u = np.zeros((nx, ny, nz))
+    for _ in range(4):
+        kx, ky, kz = rng.integers(0, 4, 3)
+        ph = rng.random(2) * 2 * np.pi
+        u += rng.random() * np.cos(np.pi * kx * x) * np.cos(2 * np.pi * ky * y + ph[0]) * \
+            np.cos(2 * np.pi * kz * z + ph[1])
+    return u + 0.25 * rng.random((nx, ny, nz))
