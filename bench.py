@@ -184,6 +184,124 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+STENCIL_BYTES_PER_CELL = 16   # one read + one write of a double per cell-step
+
+
+def run_stencil(args, rank, world, local_rank):
+    """--config G*: the stencil workload (include/dsea_grid.h) on
+    the same ring plan: metric cell-timesteps/s, roofline = HBM (16 B per cell-step)."""
+    import numpy as np
+    import torch
+    from paper_2507_11289_b200 import GRID_CONFIGS
+    from paper_2507_11289_b200 import grid as G
+    cfg = GRID_CONFIGS[args.config]
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    W = args.workers
+    g = G.Grid(cfg.nx, cfg.ny, cfg.nz, cfg.n_slices, cfg.r, n_gpus=world, rank=rank, device=local_rank,
+               workers_per_gpu=W, slices_per_stage=args.block)
+    u0 = np.random.default_rng(cfg.seed).random((cfg.nx, cfg.ny, cfg.nz))
+    if rank == 0:
+        g.set_field(u0)
+    g.connect(rank, world)
+    nw = world * W
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    barrier()
+    for _ in range(args.warmup):
+        g.step(nw)
+    barrier()
+    G.dsea_grid_reset_stats(g.g)
+    G.dsea_grid_set_timing(g.g, True)
+    hbm_peak, sm_max, peak_kind = peaks()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        g.step(args.steps * nw)
+        ev1.record()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    st = g.stats()
+    G.dsea_grid_set_timing(g.g, False)
+    t = torch.tensor([ms, float(st.kernel_launches)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+    ms_total, launches = float(t[0]), int(t[1])
+    cells = cfg.n_cells
+    value = cells * args.steps * nw / (ms_total * 1e-3)
+    per_launch_ms = st.stencil_ms / max(1, st.stencil_launches)
+    cells_per_launch = st.cell_steps / max(1, st.stencil_launches)
+    achieved = STENCIL_BYTES_PER_CELL * cells_per_launch / (per_launch_ms * 1e-3) / 1e9
+    e2e = None
+    if not args.no_e2e:
+        uh = torch.empty((cfg.nx, cfg.ny, cfg.nz), dtype=torch.float64, pin_memory=True).numpy()
+        uh[...] = u0
+        uo = torch.empty_like(torch.from_numpy(uh)).pin_memory().numpy()
+        barrier()
+        t0 = time.perf_counter()
+        if rank == 0:
+            G.dsea_grid_set_field(g.g, uh)
+        g.step(args.steps * nw)
+        if rank == 0:
+            G.lib.dsea_grid_get_field(g.g, uo.ctypes.data_as(G._pd), uo.size)
+        barrier()
+        dt = time.perf_counter() - t0
+        if dist is not None:
+            tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt[0])
+        e2e = {"value": cells * args.steps * nw / dt, "unit": "cell-timesteps/s",
+               "h2d_bytes_per_step": int(cells * 8 / args.steps), "d2h_bytes_per_step": int(cells * 8 / args.steps),
+               "note": "set_field(pinned host) + step(K super-cycles) + get_field (pinned); bytes amortised"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import grid as OG
+        slab = np.ascontiguousarray(u0[: max(8, min(cfg.nx, 64))])
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < 10.0:
+            slab = OG.ftcs_step(slab, cfg.r)
+            k += 1
+        secs = time.perf_counter() - t0
+        cpu = {"value": slab.size * k / secs, "unit": "cell-timesteps/s", "cores": 1, "kind": "oracle",
+               "sample": f"{k} numpy FTCS steps of a {slab.shape} slab of the {cfg.name} grid ({secs:.1f} s)"}
+    if rank == 0:
+        line = {
+            "metric": "cell-timesteps/s", "value": value, "unit": "cell-timesteps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded uniform random field",
+            "config": {"workload": cfg.name, "cells": [cfg.nx, cfg.ny, cfg.nz], "n_slices": cfg.n_slices,
+                       "r": cfg.r, "workers_per_gpu": W, "timesteps_per_step": nw,
+                       "mode": "fused" if world == 1 and W == 1 else "staged-ring",
+                       "l2": "inputs larger than L2 (field %.2f GB)" % (cells * 8 / 1e9),
+                       "parallelism": f"ring{world}"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None, "kernel": "k_ftcs",
+                         "bytes_per_cell": STENCIL_BYTES_PER_CELL, "peak_kind": peak_kind,
+                         "stencil_ms_per_launch": per_launch_ms},
+            "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+    g.disconnect(world)
+    g.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -202,11 +320,19 @@ def main():
                     help="NVT per-slice isokinetic thermostat at this T (P:314-316; 0 = NVE, the default)")
     args = ap.parse_args()
 
-    from paper_2507_11289_b200 import CONFIGS
-    cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config.startswith("G"):
+        if args.impl == "reference":
+            if rank == 0:
+                print(json.dumps({"impl": "reference", "unavailable": "stencil workload: use the default "
+                                  "MD workload for the reference arm"}), flush=True)
+            return
+        run_stencil(args, rank, world, local_rank)
+        return
+    from paper_2507_11289_b200 import CONFIGS
+    cfg = CONFIGS[args.config]
 
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)

@@ -5,4 +5,4 @@ MD) as sm_100a CUDA kernels behind the C ABI of include/dsea.h.
 `paper_2507_11289_b200.dsea` is the ctypes binding (same names as the C calls);
 importing it fails loudly when libdsea.so has not been built -- there is no CPU
 fallback on the product path."""
-from .configs import CONFIGS, Config  # noqa: F401
+from .configs import CONFIGS, GRID_CONFIGS, Config, GridConfig  # noqa: F401

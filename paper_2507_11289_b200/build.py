@@ -19,9 +19,10 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES_CU = ["dsea_kernels.cu"]
-SOURCES_CPP = ["dsea_host.cpp"]
-HEADERS = ["dsea_internal.h", os.path.join("..", "..", "include", "dsea.h")]
+SOURCES_CU = ["dsea_kernels.cu", "dsea_grid_kernels.cu"]
+SOURCES_CPP = ["dsea_host.cpp", "dsea_grid.cpp"]
+HEADERS = ["dsea_internal.h", "dsea_plan.h", os.path.join("..", "..", "include", "dsea.h"),
+           os.path.join("..", "..", "include", "dsea_grid.h")]
 
 
 def _nccl_include() -> str:

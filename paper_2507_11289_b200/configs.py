@@ -44,3 +44,29 @@ CONFIGS = {
     "C5e": Config("C5e", 400, 40, 32, 85, rc=4.0, cells_per_slice_x=2, note="C3 box, rc 4.0, 2 cells/slice"),
     "C5f": Config("C5f", 400, 40, 32, 56, rc=4.0, cells_per_slice_x=3, note="C3 box, rc 4.0, 3 cells/slice"),
 }
+
+
+@dataclass(frozen=True)
+class GridConfig:
+    """Stencil workload (include/dsea_grid.h): nx x ny x nz cells,
+    sliced along x into n_slices slices of nx / n_slices planes, FTCS number r."""
+    name: str
+    nx: int
+    ny: int
+    nz: int
+    n_slices: int
+    r: float = 0.1
+    seed: int = 11289
+    note: str = ""
+
+    @property
+    def n_cells(self) -> int:
+        return self.nx * self.ny * self.nz
+
+
+GRID_CONFIGS = {
+    "G0": GridConfig("G0", 48, 12, 10, 12, note="oracle-size parity: 12 slices of 4 planes, ragged tiles"),
+    "G8": GridConfig("G8", 64, 9, 40, 32, note="ring parity at 2-8 GPUs: 32 slices of 2 planes"),
+    "G1": GridConfig("G1", 512, 512, 512, 128, note="bench: 134M cells (1.07 GB per field), 128 slices "
+                     "of 4 planes (8 MB each); parallel-in-time ring at 1/2/4/8 GPUs"),
+}

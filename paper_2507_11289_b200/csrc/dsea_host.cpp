@@ -26,6 +26,7 @@
 
 #include "../../include/dsea.h"
 #include "dsea_internal.h"
+#include "dsea_plan.h"
 
 using namespace dsea;
 
@@ -104,12 +105,30 @@ PFN_writeValue32 write_value32()
     return f;
 }
 
+}  // namespace
+
+namespace dsea {
+int stream_wait_geq32(cudaStream_t s, const uint32_t* addr, uint32_t v)
+{
+    return wait_value32() ? wait_value32()(s, (unsigned long long)addr, v, 0) : -1;
+}
+int stream_write32(cudaStream_t s, uint32_t* addr, uint32_t v)
+{
+    return write_value32() ? write_value32()(s, (unsigned long long)addr, v, 0) : -1;
+}
+bool stream_memops_available() { return wait_value32() && write_value32(); }
+}  // namespace dsea
+
+namespace {
 struct PeerBlob {
     int32_t magic, rank, ns, pad;
     cudaIpcMemHandle_t in, arr, rel;
 };
 constexpr int32_t PEER_MAGIC = 0x44534541;  // "DSEA"
 
+}  // namespace
+
+namespace dsea {
 // ------------------------------------------------------------------------------
 // Stage schedule (Table 1 generalised).  The slices of a super-cycle are grouped in
 // blocks of B consecutive slices (B = 1 is the paper's schedule); flat blocks
@@ -123,23 +142,6 @@ constexpr int32_t PEER_MAGIC = 0x44534541;  // "DSEA"
 // that timestep is beyond the requested count (Q15).  For B = 1 this is exactly
 // Table 1: receive k, process k-2, send k-3.
 // ------------------------------------------------------------------------------
-enum OpKind { OP_RECV = 0, OP_FORCE, OP_PASS, OP_BIN, OP_SEND };
-
-struct Op {
-    int kind;
-    int stage;
-    int worker;
-    int slice;      // first slice
-    int count;      // number of consecutive slices
-    int cycle;
-    int64_t t_rel;  // timestep relative to the start of the call (FORCE only)
-};
-
-struct Plan {
-    std::vector<Op> ops;
-    int n_stages = 0;
-};
-
 // Partition of the N_S slices into the blocks of a super-cycle: nblk = ceil(N_S / B)
 // blocks of balanced size (sizes differ by at most one slice, so no short tail block:
 // a one-slice tail block cost up to 4 % on the C4 ring, profiles/r01/ring_tuning).
@@ -148,14 +150,6 @@ struct Plan {
 // instead of 2 B.  Measured on 4 B200s (C4, B = 7): 0.9 % slower -- the steady-state
 // lag between ranks is two blocks of the current size, so the earlier start only turns
 // into a stall at the first full-size block and the drain keeps the full lag.
-struct Blocks {
-    std::vector<int> first;   // nblk + 1 entries, first[nblk] = ns
-    std::vector<int> of;      // block of each slice
-    int d = 1;                // worker w+1 trails worker w by d stages
-    int n() const { return (int)first.size() - 1; }
-    int count(int c) const { return first[c + 1] - first[c]; }
-};
-
 Blocks make_blocks(int ns, int ng, int B)
 {
     Blocks bl;
@@ -176,8 +170,6 @@ Blocks make_blocks(int ns, int ng, int B)
     return bl;
 }
 
-bool plan_plateau(int ng, int W, const Blocks& bl);
-int plan_gap(int ng, int W, const Blocks& bl);
 
 Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps, const Blocks& bl)
 {
@@ -289,6 +281,9 @@ int plan_gap(int ng, int W, const Blocks& bl)
 {
     return plan_plateau(ng, W, bl) ? bl.d * (W - 1) : 0;
 }
+}  // namespace dsea
+
+namespace {
 }  // namespace
 
 // ------------------------------------------------------------------------------

@@ -25,6 +25,42 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(D.lib, name)
 
 
+def test_library_exports_every_grid_symbol():
+    """include/dsea_grid.h (the stencil workload): every declaration is exported by
+    libdsea.so and bound, under the same name, by paper_2507_11289_b200.grid."""
+    from paper_2507_11289_b200 import grid as G
+    hdr = open(os.path.join(ROOT, "include", "dsea_grid.h")).read()
+    declared = set(re.findall(r"^\s*(?:dsea_status|void|const char \*)\s*(dsea_grid_\w+)\s*\(", hdr, re.M))
+    assert len(declared) == 12
+    assert declared == {name for name, _, _ in G.SIGNATURES}
+    for name in declared:
+        assert hasattr(D.lib, name)
+
+
+@pytest.mark.parametrize("kw", [dict(nx=10, n_slices=4), dict(r=0.2), dict(r=0.0), dict(ny=2), dict(n_slices=2),
+                                dict(rank=2, n_gpus=2), dict(workers_per_gpu=0), dict(mode=1, n_gpus=2),
+                                dict(slices_per_stage=13)])
+def test_grid_create_rejects_bad_parameters(kw):
+    """Parameter validation happens on the host before any device call (DSEA_EINVAL);
+    valid parameters on a machine without a GPU give DSEA_ECUDA (no CPU fallback)."""
+    from paper_2507_11289_b200 import grid as G
+    p = dict(nx=12, ny=4, nz=5, n_slices=12, r=0.1)
+    p.update(kw)
+    with pytest.raises(D.DseaError) as e:
+        G.dsea_grid_create(**p)
+    assert e.value.status == D.DSEA_EINVAL
+
+
+def test_grid_create_without_gpu_is_ecuda():
+    import torch
+    from paper_2507_11289_b200 import grid as G
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(D.DseaError) as e:
+        G.dsea_grid_create(12, 4, 5, 12, 0.1)
+    assert e.value.status == D.DSEA_ECUDA
+
+
 @pytest.mark.parametrize("name", ["C1", "P8", "C2", "C3", "C4", "C5b", "C5f"])
 def test_geometry_matches_oracle(name):
     """dsea_geometry_compute (Q3) equals the oracle's geometry bit for bit."""
