@@ -340,6 +340,15 @@ struct dsea_ctx {
     uint32_t* succ_arr = nullptr;       // mapped successor arrival flags
     uint32_t* pred_rel = nullptr;       // mapped predecessor release flags
     std::vector<uint32_t> wr_cnt, exp_arr, rel_cnt;
+    // copy-engine hop: monotone counters instead of per-slot flags (as the stencil
+    // engine, dsea_grid.cpp): slots arrive / are released in (super-cycle, slot)
+    // order, so the k-th arrival (release) of slot s is event (k-1) N_S + s + 1; one
+    // stream memory op per hop / release instead of one per slot, and no release
+    // kernel on the compute stream.  arr_dev[0] / rel_dev[0] hold the counters.
+    bool ctr = false;
+    uint32_t rel_init = 0;                          // successor's slots start occupied (it is rank 0)
+    std::vector<uint32_t> push_k, rel_k;            // per slot: pushes made, releases made
+    cudaEvent_t ev_bs = nullptr;                    // last push on the hop stream
     char* own_outb_last = nullptr;      // locally allocated last output buffer (unused when peer)
 
     // host mirror of the device state (rank 0), valid until the next mutation
@@ -538,6 +547,8 @@ void free_device(dsea_ctx* c)
     c->ev_hop.clear();
     c->hop_rec.clear();
     if (c->ev_cs) cudaEventDestroy(c->ev_cs);
+    if (c->ev_bs) cudaEventDestroy(c->ev_bs);
+    c->ev_bs = nullptr;
     c->ev_cs = nullptr;
     c->bs = nullptr;
     for (cudaEvent_t e : c->ev_force) cudaEventDestroy(e);
@@ -721,9 +732,34 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
     NcclApi& api = nccl();
     const int W = c->W;
     auto in_of = [&](int w) -> BufView& { return w == 0 ? c->inb : c->outb[w - 1]; };
-    const size_t nops = P.ops.size();
+    // counter mode (c->ctr): event number of the k-th arrival / release of slot s
+    auto ev_no = [&](uint32_t k, int s) { return (k - 1) * (uint32_t)ns + (uint32_t)s + 1; };
+    auto wait_arrival = [&](int s) -> dsea_status {
+        const bool ok = c->ctr ? stream_wait_geq32(c->cs, c->arr_dev, ev_no(c->exp_arr[s], s)) == 0
+                               : wait_value32()(c->cs, (unsigned long long)(c->arr_dev + s), c->exp_arr[s], 0) == 0;
+        return ok ? DSEA_OK : fail(c, DSEA_EPEER, "cuStreamWaitValue32 (arrival) failed");
+    };
+    auto release_ctr = [&](int f0, int f1) -> dsea_status {   // slots [f0, f1] read for the last time
+        if (f1 < f0) return DSEA_OK;
+        for (int sl = f0; sl <= f1; sl++) c->rel_k[sl]++;
+        if (stream_write32(c->cs, c->pred_rel, ev_no(c->rel_k[f1], f1)))
+            return fail(c, DSEA_EPEER, "cuStreamWriteValue32 (release) failed");
+        return DSEA_OK;
+    };
+    // counter mode: pushes must leave in (super-cycle, slot) order -- where the plan
+    // lists PASS(block 0 of cycle K) before BIN(last slice of K-1) for the last worker,
+    // that BIN (data binned in an earlier stage) runs first
+    std::vector<Op> ops = P.ops;
+    if (c->ctr)
+        for (size_t i = 0; i + 1 < ops.size(); i++)
+            if (ops[i].kind == OP_PASS && ops[i].worker == W - 1)
+                for (size_t k = i + 1; k < ops.size() && ops[k].stage == ops[i].stage &&
+                                       ops[k].worker == ops[i].worker && ops[k].kind == OP_BIN;
+                     k++)
+                    if (ops[k].cycle < ops[i].cycle) std::rotate(ops.begin() + i, ops.begin() + k, ops.begin() + k + 1), i++;
+    const size_t nops = ops.size();
     for (size_t oi = 0; oi < nops; oi++) {
-        const Op& op = P.ops[oi];
+        const Op& op = ops[oi];
         switch (op.kind) {
         case OP_RECV: {
             if (c->peer) {  // data arrives by remote stores; just count the expected arrival
@@ -733,18 +769,18 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             // all receives of this stage in one NCCL group (matched by order with the
             // predecessor's sends, one message per slice)
             size_t oe = oi;
-            while (oe < nops && P.ops[oe].kind == OP_RECV && P.ops[oe].stage == op.stage) oe++;
+            while (oe < nops && ops[oe].kind == OP_RECV && ops[oe].stage == op.stage) oe++;
             for (size_t q = oi; q < oe; q++)
-                CUDA_TRY(c, cudaStreamWaitEvent(c->rs, c->ev_free[P.ops[q].slice], 0));
+                CUDA_TRY(c, cudaStreamWaitEvent(c->rs, c->ev_free[ops[q].slice], 0));
             api.GroupStart();
             for (size_t q = oi; q < oe; q++) {
-                ncclResult_t r = api.Recv(c->inb.base + (size_t)P.ops[q].slice * sb, sb, ncclChar, 0,
+                ncclResult_t r = api.Recv(c->inb.base + (size_t)ops[q].slice * sb, sb, ncclChar, 0,
                                           c->recv_comm, c->rs);
                 if (r != ncclSuccess) { api.GroupEnd(); return fail(c, DSEA_EPEER, "ncclRecv: %s", api.GetErrorString(r)); }
             }
             ncclResult_t r = api.GroupEnd();
             if (r != ncclSuccess) return fail(c, DSEA_EPEER, "ncclGroupEnd (recv): %s", api.GetErrorString(r));
-            for (size_t q = oi; q < oe; q++) CUDA_TRY(c, cudaEventRecord(c->ev_recv[P.ops[q].slice], c->rs));
+            for (size_t q = oi; q < oe; q++) CUDA_TRY(c, cudaEventRecord(c->ev_recv[ops[q].slice], c->rs));
             oi = oe - 1;
             break;
         }
@@ -753,8 +789,8 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             if (w == 0 && c->NG > 1 && !(c->rank == 0 && op.cycle == 0)) {
                 const int need = std::min(j + n, ns - 1);   // right neighbour of the block
                 if (c->peer) {
-                    if (wait_value32()(c->cs, (unsigned long long)(c->arr_dev + need), c->exp_arr[need], 0))
-                        return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (arrival) failed");
+                    dsea_status s = wait_arrival(need);
+                    if (s) return s;
                 } else {
                     CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[need], 0));
                 }
@@ -792,7 +828,10 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             if (w == 0 && c->NG > 1) {
                 // slot s is last read by the unit of slice s+1
                 const int f0 = std::max(j - 1, 0), f1 = (j + n == ns) ? ns - 1 : j + n - 2;
-                if (c->peer) {
+                if (c->ctr) {
+                    dsea_status s = release_ctr(f0, f1);
+                    if (s) return s;
+                } else if (c->peer) {
                     if (f1 >= f0) {  // release the slots to the predecessor (one count per cycle)
                         const uint32_t v = ++c->rel_cnt[f0];
                         for (int sl = f0 + 1; sl <= f1; sl++) c->rel_cnt[sl] = v;
@@ -809,11 +848,39 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             const int j = op.slice, n = op.count, w = op.worker;
             if (w == 0 && c->NG > 1 && !(c->rank == 0 && op.cycle == 0)) {
                 if (c->peer) {
-                    if (wait_value32()(c->cs, (unsigned long long)(c->arr_dev + j + n - 1), c->exp_arr[j + n - 1], 0))
-                        return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (arrival) failed");
+                    dsea_status s = wait_arrival(j + n - 1);
+                    if (s) return s;
                 } else {
                     CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_recv[j + n - 1], 0));
                 }
+            }
+            if (c->ctr && w == W - 1 && c->NG > 1) {
+                // push on the compute stream after every earlier push (hop stream) has
+                // left, so the arrival counter stays in slot order
+                CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_bs, 0));
+                for (int sl = j; sl < j + n; sl++) c->push_k[sl]++;
+                const uint32_t need = c->push_k[j + n - 1] - 1 + c->rel_init;
+                if (need > 0 && stream_wait_geq32(c->cs, c->rel_dev, ev_no(need, j + n - 1)))
+                    return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (release) failed");
+                CUDA_TRY(c, cudaMemcpyAsync(c->succ_in_base + (size_t)j * sb, in_of(w).base + (size_t)j * sb, sb * n,
+                                            cudaMemcpyDeviceToDevice, c->cs));
+                if (stream_write32(c->cs, c->succ_arr, ev_no(c->push_k[j + n - 1], j + n - 1)))
+                    return fail(c, DSEA_EPEER, "cuStreamWriteValue32 (arrival) failed");
+                CUDA_TRY(c, cudaEventRecord(c->ev_bs, c->cs));
+                if (w == 0) {
+                    dsea_status s = release_ctr(j, j + n - 1);
+                    if (s) return s;
+                }
+                break;
+            }
+            if (c->ctr && w == 0 && c->NG > 1) {       // (w < W-1: local copy, then release)
+                BufView& src0 = in_of(0);
+                if (src0.base != c->outb[0].base)
+                    CUDA_TRY(c, cudaMemcpyAsync(c->outb[0].base + (size_t)j * sb, src0.base + (size_t)j * sb, sb * n,
+                                                cudaMemcpyDeviceToDevice, c->cs));
+                dsea_status s = release_ctr(j, j + n - 1);
+                if (s) return s;
+                break;
             }
             uint32_t wv = 0;
             if (w == W - 1 && c->NG > 1) {
@@ -858,6 +925,7 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 const int nblk = c->bl.n();
                 for (int k = c->bl.of[m]; k <= c->bl.of[m + n - 1]; k++)   // previous push of these slots
                     if (c->hop_rec[k]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_hop[k], 0));
+                (void)nblk;
                 cudaEvent_t t0 = nullptr, t1 = nullptr;
                 if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
                 const int s0 = std::max(m - 1, 0), s1 = std::min(m + n, ns - 1);
@@ -871,16 +939,29 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 for (int sl = m + 1; sl < m + n; sl++) c->wr_cnt[sl] = wv;
                 CUDA_TRY(c, cudaEventRecord(c->ev_cs, c->cs));
                 CUDA_TRY(c, cudaStreamWaitEvent(c->bs, c->ev_cs, 0));
-                for (int sl = m; sl < m + n; sl++)   // the successor released the previous occupants
-                    if (wait_value32()(c->bs, (unsigned long long)(c->rel_dev + sl), wv, 0))
+                if (c->ctr) {                        // one wait on the successor's release counter
+                    for (int sl = m; sl < m + n; sl++) c->push_k[sl]++;
+                    const uint32_t need = c->push_k[m + n - 1] - 1 + c->rel_init;
+                    if (need > 0 && stream_wait_geq32(c->bs, c->rel_dev, ev_no(need, m + n - 1)))
                         return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (release) failed");
+                } else {
+                    for (int sl = m; sl < m + n; sl++)   // the successor released the previous occupants
+                        if (wait_value32()(c->bs, (unsigned long long)(c->rel_dev + sl), wv, 0))
+                            return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (release) failed");
+                }
                 cudaEvent_t h0 = nullptr, h1 = nullptr;
                 if (c->timing) { h0 = tev(c); h1 = tev(c); cudaEventRecord(h0, c->bs); }
                 CUDA_TRY(c, cudaMemcpyAsync(c->succ_in_base + (size_t)m * sb, ob.base + (size_t)m * sb, sb * n,
                                             cudaMemcpyDeviceToDevice, c->bs));
-                for (int sl = m; sl < m + n; sl++)
-                    if (write_value32()(c->bs, (unsigned long long)(c->succ_arr + sl), wv, 0))
+                if (c->ctr) {
+                    if (stream_write32(c->bs, c->succ_arr, ev_no(c->push_k[m + n - 1], m + n - 1)))
                         return fail(c, DSEA_EPEER, "cuStreamWriteValue32 (arrival) failed");
+                    CUDA_TRY(c, cudaEventRecord(c->ev_bs, c->bs));
+                } else {
+                    for (int sl = m; sl < m + n; sl++)
+                        if (write_value32()(c->bs, (unsigned long long)(c->succ_arr + sl), wv, 0))
+                            return fail(c, DSEA_EPEER, "cuStreamWriteValue32 (arrival) failed");
+                }
                 if (c->timing) { cudaEventRecord(h1, c->bs); c->tpairs.push_back({TK_SEND, {h0, h1}}); }
                 const int key = c->bl.of[m + n - 1] % nblk;
                 CUDA_TRY(c, cudaEventRecord(c->ev_hop[key], c->bs));
@@ -934,16 +1015,16 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
         }
         case OP_SEND: {
             size_t oe = oi;
-            while (oe < nops && P.ops[oe].kind == OP_SEND && P.ops[oe].stage == op.stage) oe++;
+            while (oe < nops && ops[oe].kind == OP_SEND && ops[oe].stage == op.stage) oe++;
             // ring of one: written into the input buffer; peer: written into the successor
             if (c->NG == 1 || c->peer) { oi = oe - 1; break; }
             for (size_t q = oi; q < oe; q++)
-                CUDA_TRY(c, cudaStreamWaitEvent(c->ss, c->ev_bin[P.ops[q].slice], 0));
+                CUDA_TRY(c, cudaStreamWaitEvent(c->ss, c->ev_bin[ops[q].slice], 0));
             cudaEvent_t t0 = nullptr, t1 = nullptr;
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->ss); }
             api.GroupStart();
             for (size_t q = oi; q < oe; q++) {
-                ncclResult_t r = api.Send(c->outb[W - 1].base + (size_t)P.ops[q].slice * sb, sb, ncclChar, 1,
+                ncclResult_t r = api.Send(c->outb[W - 1].base + (size_t)ops[q].slice * sb, sb, ncclChar, 1,
                                           c->send_comm, c->ss);
                 if (r != ncclSuccess) { api.GroupEnd(); return fail(c, DSEA_EPEER, "ncclSend: %s", api.GetErrorString(r)); }
             }
@@ -951,8 +1032,8 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             if (r != ncclSuccess) return fail(c, DSEA_EPEER, "ncclGroupEnd (send): %s", api.GetErrorString(r));
             if (c->timing) { cudaEventRecord(t1, c->ss); c->tpairs.push_back({TK_SEND, {t0, t1}}); }
             for (size_t q = oi; q < oe; q++) {
-                CUDA_TRY(c, cudaEventRecord(c->ev_send[P.ops[q].slice], c->ss));
-                sent[P.ops[q].slice] = 1;
+                CUDA_TRY(c, cudaEventRecord(c->ev_send[ops[q].slice], c->ss));
+                sent[ops[q].slice] = 1;
                 c->stats.hop_bytes += (int64_t)sb;
             }
             oi = oe - 1;
@@ -961,9 +1042,16 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
         }
     }
     if (c->peer && c->rank == 0) {  // the final super-cycle lands in rank 0's input buffer
-        for (int sl = 0; sl < ns; sl++)
-            if (wait_value32()(c->cs, (unsigned long long)(c->arr_dev + sl), c->exp_arr[sl], 0))
-                return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (final arrival) failed");
+        if (c->ctr) {
+            if (c->exp_arr[ns - 1] > 0) {
+                dsea_status s = wait_arrival(ns - 1);
+                if (s) return s;
+            }
+        } else {
+            for (int sl = 0; sl < ns; sl++)
+                if (wait_value32()(c->cs, (unsigned long long)(c->arr_dev + sl), c->exp_arr[sl], 0))
+                    return fail(c, DSEA_EPEER, "cuStreamWaitValue32 (final arrival) failed");
+        }
     }
     return DSEA_OK;
 }
@@ -1299,6 +1387,15 @@ dsea_status dsea_ring_connect_peer(dsea_ctx* c, const void* blobs, size_t blob_b
     // or SM remote stores (DSEA_PEER_HOP=sm: the bin kernels write the successor's slots)
     const char* hop = getenv("DSEA_PEER_HOP");
     c->ce_hop = !(hop && std::strcmp(hop, "sm") == 0);
+    const char* ctr = getenv("DSEA_RING_COUNTERS");      // A/B: 0 = per-slot flags
+    c->ctr = c->ce_hop && !(ctr && *ctr && atoi(ctr) == 0);
+    if (c->ctr) {
+        CUDA_TRY(c, cudaMemset(c->rel_dev, 0, sizeof(uint32_t) * ns));
+        c->rel_init = succ == 0 ? 1u : 0u;
+        c->push_k.assign(ns, 0u);
+        c->rel_k.assign(ns, 0u);
+        if (!c->ev_bs) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_bs, cudaEventDisableTiming));
+    }
     if (c->ce_hop && !write_value32()) return fail(c, DSEA_EPEER, "cuStreamWriteValue32 unavailable");
     if (!c->ce_hop) {
         // the last worker's output buffer is the successor's input buffer (local scratch kept)
