@@ -14,9 +14,17 @@
 
 namespace dsea {
 
-constexpr int FTCS_TZ = 32;      // threads along z (one warp row: coalesced)
-constexpr int FTCS_TY = 8;       // rows along y
-constexpr int FTCS_XCHUNK = 16;  // planes marched by one CTA
+// tile shape swept on B200 (G1, 512^3): 32 x 4 x 32 planes 4.07 TB/s; 32 x 8 x 16
+// 3.97; 32 x 8 x 32 4.02; 32 x 8 x 64 3.93; 32 x 16 x 8 3.69
+#ifndef DSEA_FTCS_TY
+#define DSEA_FTCS_TY 4
+#endif
+#ifndef DSEA_FTCS_XCHUNK
+#define DSEA_FTCS_XCHUNK 32
+#endif
+constexpr int FTCS_TZ = 32;                 // threads along z (one warp row: coalesced)
+constexpr int FTCS_TY = DSEA_FTCS_TY;       // rows along y
+constexpr int FTCS_XCHUNK = DSEA_FTCS_XCHUNK;  // planes marched by one CTA
 
 __device__ __forceinline__ void pdl_wait_g() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_release_g() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -25,7 +33,8 @@ __device__ __forceinline__ void pdl_release_g() { asm volatile("griddepcontrol.l
 // the y/z neighbours are the same plane's values loaded by the tile's other threads
 // (L1 hits).  Staging the plane tile in shared memory instead (two CTA barriers per
 // plane) measured slower on B200: 3.15 vs 3.97 TB/s, and so did loading the next
-// plane one iteration ahead: 3.71 TB/s.
+// plane one iteration ahead (3.71 TB/s) and two interleaved x-marches per thread
+// (3.84-3.96 TB/s).
 __global__ void __launch_bounds__(FTCS_TZ* FTCS_TY)
 k_ftcs(const double* __restrict__ in, double* __restrict__ out, int x0, int x1, int nx, int ny, int nz,
        double r)
