@@ -221,3 +221,89 @@ def test_gloo_ring_emulation_equals_sequential():
     d[:, 1:] -= g.b[1:] * np.round(d[:, 1:] / g.b[1:])
     assert np.max(np.abs(d)) < 1e-12
     assert np.max(np.abs(final[:, 4:7] - vo)) < 1e-11
+
+
+# ---------------------------------------------------------------- 4. stencil ring emulation
+# The second workload (include/dsea_grid.h: O_in = 1, O_out = 0) on two
+# gloo ranks, executing the shared stage plan (dsea_plan_ops) op by op the way
+# dsea_grid.cpp does: FORCE = the oracle FTCS step of a block's planes from the
+# worker's input buffer into its output buffer; BIN = the last worker pushes the
+# finished slices to the successor (one message per slice); PASS = copy through /
+# push (partial super-cycles, Q15).  Pushes leave in (super-cycle, slot) order: a BIN
+# of the previous cycle listed after a PASS of the same stage goes first (the rule
+# dsea_grid.cpp applies for its monotone counters).  Receives are consumed lazily, in
+# order, when a worker-0 op needs a slot.  The field on rank 0 must equal the
+# sequential oracle run bit for bit.
+GNX, GNY, GNZ, GNS, GR = 24, 4, 5, 12, 0.12
+R_, F_, P_, BN_, S_ = D.OP_RECV, D.OP_FORCE, D.OP_PASS, D.OP_BIN, D.OP_SEND
+
+
+def _grid_ring_worker(rank, world, W, B, n_steps, calls):
+    from oracle import grid as OG
+    from tests import inputs
+    p = GNX // GNS
+    u0 = inputs.grid_field(GNX, GNY, GNZ, 3)
+    inb = u0.copy() if rank == 0 else np.zeros_like(u0)
+    outb = [np.zeros_like(u0) for _ in range(W)]
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+    pending, queue = [], []          # isend handles; expected receives (slot) in order
+    got = {}                          # slot -> times received
+
+    expected = {}                     # slot -> receptions the plan has announced so far
+
+    def recv_until(slot):
+        while got.get(slot, 0) < expected.get(slot, 0):
+            s = queue.pop(0)
+            buf = np.zeros((p, GNY, GNZ))
+            dist.recv(_t(buf), src=prv)
+            inb[s * p:(s + 1) * p] = buf
+            got[s] = got.get(s, 0) + 1
+
+    def push(src, m, n):
+        for s in range(m, m + n):
+            pending.append(dist.isend(_t(np.ascontiguousarray(src[s * p:(s + 1) * p])), dst=nxt))
+
+    per = n_steps // calls
+    for call in range(calls):
+        steps = per if call < calls - 1 else n_steps - per * (calls - 1)
+        ops = [tuple(int(v) for v in o) for o in D.dsea_plan_ops(GNS, world, rank, W, steps, B)]
+        for i in range(len(ops) - 1):   # push order rule (see above)
+            if ops[i][0] == P_ and ops[i][2] == W - 1:
+                k = i + 1
+                while k < len(ops) and ops[k][1] == ops[i][1] and ops[k][2] == ops[i][2] and ops[k][0] == BN_:
+                    if ops[k][5] < ops[i][5]:
+                        ops.insert(i, ops.pop(k))
+                        i += 1
+                    k += 1
+        for kind, stage, w, j, n, K, t in ops:
+            if kind == R_:
+                queue.append(j)
+                expected[j] = expected.get(j, 0) + 1
+            elif kind in (F_, P_):
+                src = inb if w == 0 else outb[w - 1]
+                if w == 0:
+                    recv_until(min(j + n, GNS - 1) if kind == F_ else j + n - 1)
+                if kind == F_:
+                    lo, hi = max(j * p - 1, 0), min((j + n) * p + 1, GNX)
+                    res = OG.ftcs_step(src[lo:hi], GR)
+                    outb[w][j * p:(j + n) * p] = res[j * p - lo:j * p - lo + n * p]
+                elif w == W - 1:
+                    push(src, j, n)
+                else:
+                    outb[w][j * p:(j + n) * p] = src[j * p:(j + n) * p]
+            elif kind == BN_ and w == W - 1:
+                push(outb[W - 1], j, n)
+        if rank == 0:                 # the final super-cycle lands on rank 0
+            recv_until(GNS - 1)
+    for h in pending:
+        h.wait()
+    return inb if rank == 0 else "ok"
+
+
+@pytest.mark.parametrize("W,B,n_steps,calls", [(1, 2, 6, 1), (1, 3, 7, 2), (2, 1, 8, 1), (2, 4, 9, 2), (1, 1, 5, 1)])
+def test_gloo_stencil_ring_emulation_equals_sequential(W, B, n_steps, calls):
+    from oracle import grid as OG
+    from tests import inputs
+    res = _spawn(_grid_ring_worker, 2, W, B, n_steps, calls)
+    u0 = inputs.grid_field(GNX, GNY, GNZ, 3)
+    assert np.array_equal(res[0], OG.run(u0, GR, n_steps))
