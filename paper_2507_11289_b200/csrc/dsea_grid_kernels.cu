@@ -14,13 +14,16 @@
 
 namespace dsea {
 
-// tile shape swept on B200 (G1, 512^3): 32 x 4 x 32 planes 4.07 TB/s; 32 x 8 x 16
-// 3.97; 32 x 8 x 32 4.02; 32 x 8 x 64 3.93; 32 x 16 x 8 3.69
+// tile shape swept on B200 (G1, 512^3, one full sweep): 32 x 4 x 32 planes 4.07 TB/s;
+// 32 x 8 x 16 3.97; 32 x 8 x 32 4.02; 32 x 8 x 64 3.93; 32 x 16 x 8 3.69.  The ring's
+// per-block launches cover only a few slices, where 32-plane chunks leave too few CTAs
+// (ring of 4, W = 2: 4.16e11 vs 4.67e11 cell-steps/s), so the default is 32 x 8 x 16
+//
 #ifndef DSEA_FTCS_TY
-#define DSEA_FTCS_TY 4
+#define DSEA_FTCS_TY 8
 #endif
 #ifndef DSEA_FTCS_XCHUNK
-#define DSEA_FTCS_XCHUNK 32
+#define DSEA_FTCS_XCHUNK 16
 #endif
 constexpr int FTCS_TZ = 32;                 // threads along z (one warp row: coalesced)
 constexpr int FTCS_TY = DSEA_FTCS_TY;       // rows along y
