@@ -79,7 +79,11 @@ typedef struct {
     int32_t slices_per_stage;  /* B >= 1 consecutive slices handled per stage (B = 1 is the
                                   paper's Table 1 schedule); 0 -> auto: enough atoms per
                                   launch, while keeping >= N_GPU*(2+W) blocks per super-cycle */
-    double capacity_factor;    /* slot capacity / mean atoms per slice; 0 -> 1.25 */
+    double capacity_factor;    /* slot capacity / mean atoms per slice; 0 -> 1.25.  Above
+                                  1.25 it declares regions denser than the mean (an
+                                  inhomogeneous state): the force tiles' shared-memory
+                                  staging is sized for capacity_factor / 1.25 x the mean
+                                  density too */
 } dsea_slice_params;
 
 #define DSEA_MODE_AUTO 0   /* FUSED when n_gpus == 1 and W == 1, else STAGED */

@@ -1231,7 +1231,10 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
 
     int optin = 0;
     CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, sp->device));
-    const double mean_per_cell = (double)c->N / ((double)g.ns * g.ncell);
+    // a capacity factor above the default declares denser regions than the mean: the
+    // force tiles' shared-memory staging is sized for them too
+    const double dens_scale = std::max(1.0, (sp->capacity_factor > 0 ? sp->capacity_factor : 1.25) / 1.25);
+    const double mean_per_cell = dens_scale * (double)c->N / ((double)g.ns * g.ncell);
     c->T = choose_tiling(g, mean_per_cell, optin);
     const int per_sm = force_kernel_attr(c->T);
     if (per_sm < 1) return fail(c, DSEA_ECUDA, "cannot set %zu bytes of dynamic shared memory", c->T.smem);

@@ -344,3 +344,29 @@ def test_overfull_cell_binned_exactly():
     _cells_exact(e, c)
     cg, _ = e.cells()
     assert np.sum(np.all(cg == [2, 2, 2], axis=1)) >= 100
+
+
+@pytest.mark.parametrize("mode,W,B", [(D.DSEA_MODE_FUSED, 1, 0), (D.DSEA_MODE_STAGED, 2, 3)])
+def test_empty_slices(mode, W, B):
+    """Edge case: half the slices hold no atoms.  A rho = 0.3 box (P8 shape) whose lattice
+    is compressed into the left half along x (local density 0.6): slices 16-31 are
+    empty, the occupied ones hold twice the mean (capacity_factor 3).  Forces, positions
+    after 5 steps and cells against the oracle (Q13, Q14, Q4), in the fused pass and on
+    a staged ring of one."""
+    from paper_2507_11289_b200 import Config
+    c = Config("E", 48, 5, 5, 32, rho=0.3)
+    g = _geom(c)
+    x = oracle.lattice(c.nx, c.ny, c.nz, g.a)
+    x[:, 0] *= 0.5
+    v = inputs.gaussian_velocities(c.n_atoms, 0.3, 4)
+    e, _ = _engine(c, mode=mode, workers_per_gpu=W, slices_per_stage=B, capacity_factor=3.0)
+    e.set_state(x, v)
+    _, sl = e.cells()
+    assert sl.max() < c.n_slices // 2 + 1
+    e.step(5)
+    xo, vo, Fo, _ = oracle.run(x, v, np.zeros_like(x), g.b, c.rc, c.dt, 5)
+    _force_close(e.forces(), Fo)
+    d = _min_image(e.positions() - xo, g.b)
+    assert np.abs(d).max() <= 1e-8
+    _cells_exact(e, c)
+    e.close()
