@@ -314,7 +314,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--hop", default="peer", choices=["peer", "nccl"],
-                    help="ring hop: fused NVLink remote stores (peer) or NCCL send/recv")
+                    help="ring hop: NVLink copy-engine push with stream flags (peer) or NCCL send/recv")
     ap.add_argument("--block", type=int, default=0, help="slices per stage (0 = auto)")
     ap.add_argument("--thermostat", type=float, default=0.0,
                     help="NVT per-slice isokinetic thermostat at this T (P:314-316; 0 = NVE, the default)")
