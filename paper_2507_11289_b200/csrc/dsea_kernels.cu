@@ -57,14 +57,23 @@ __device__ __forceinline__ int32_t* slot_i(const BufView& B, int j, size_t off) 
     return reinterpret_cast<int32_t*>(B.base + (size_t)j * B.L.slot_bytes + off);
 }
 
-// 1/x in FP64: MUFU approximation + two Newton steps (relative error ~1e-16).
+// 1/x in FP64: MUFU approximation + Newton steps.  One step (default) leaves a relative
+// error of ~2^-45 in 1/r^2 -- about 1e-13 in a pair force, far inside the 1e-10 parity
+// bound (Q13) -- and shortens each hit's dependent FP64 chain by two DFMAs (C4 force
+// launch 10.09 -> 9.93 ms); -DDSEA_RCP_NEWTON=2 restores the correctly-rounded-like
+// reciprocal.
+#ifndef DSEA_RCP_NEWTON
+#define DSEA_RCP_NEWTON 1
+#endif
 __device__ __forceinline__ double rcp64(double x) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     double e = fma(-x, y, 1.0);
     y = fma(y, e, y);
+#if DSEA_RCP_NEWTON >= 2
     e = fma(-x, y, 1.0);
     y = fma(y, e, y);
+#endif
     return y;
 }
 
