@@ -6,8 +6,12 @@
 //  - FCC lattice + velocities .... P:224-227 §4 (Q9, Q10); host, -ffp-contract=off
 //  - stage schedule .............. Table 1 (§3.3) generalised to W workers
 //                                  per GPU and N_GPU GPUs in a ring
-//  - ring hop .................... P:118-119 §3.1, §3.4: NCCL point-to-point
-//                                  over NVLink, one process per GPU
+//  - ring hop .................... P:118-119 §3.1, §3.4: one process per GPU;
+//                                  default: copy-engine push over NVLink into the
+//                                  successor's CUDA-IPC-mapped input slots, monotone
+//                                  arrival/release counters as stream flags; NCCL
+//                                  point-to-point and SM remote stores as comparisons
+//  - stage plan .................. dsea_plan.h (shared with the stencil engine)
 //  - super-cycle ................. P:89-92 §3.1
 #include <cuda_runtime.h>
 #include <dlfcn.h>
