@@ -65,6 +65,7 @@ __device__ __forceinline__ int32_t* slot_i(const BufView& B, int j, size_t off) 
 #ifndef DSEA_RCP_NEWTON
 #define DSEA_RCP_NEWTON 1
 #endif
+
 __device__ __forceinline__ double rcp64(double x) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -918,10 +919,15 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                     const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
                     if (r2 <= rc2 && kk != si) {      // inclusive cutoff; i != j
                         const double s = rcp64(r2);
-                        const double s3 = s * s * s;
-                        const double t = fma(2.0, s3, -1.0);
-                        const double gq = s3 * t;
-                        const double f = s * gq;
+                        // f = s^4 (2 s^3 - 1) with s^4 = (s^2)^2 formed beside s^3: one
+                        // dependent multiply less on each hit's force chain than s (s^3 t)
+                        // (C4 force launch -0.65 %); gq = s^3 t feeds only the virial
+                        const double s2 = s * s;
+                        const double s3 = s2 * s;                  // r^-6
+                        const double s4 = s2 * s2;
+                        const double t = fma(2.0, s3, -1.0);       // 2 r^-6 - 1
+                        const double gq = s3 * t;                  // 2 r^-12 - r^-6
+                        const double f = s4 * t;                   // F_abs / 24
                         fx = fma(dx, f, fx);
                         fy = fma(dy, f, fy);
                         fz = fma(dz, f, fz);
