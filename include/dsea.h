@@ -269,6 +269,8 @@ dsea_status dsea_schedule(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_
  * stream order.  Each row is 7 int32: {kind (0 recv, 1 force, 2 pass-through,
  * 3 bin/finalise, 4 send), stage, worker (-1 for recv), first slice (0-based),
  * slice count, super-cycle, timestep relative to the call (force; else -1)}.
+ * The list is in the order the default (copy-engine) ring executes it: pushes to the
+ * successor leave in (super-cycle, slot) order.
  * rows = NULL queries the count into *n_rows.  Host only; used by the CPU tests to
  * check the cross-rank dependency order (no deadlock, every unit once). */
 dsea_status dsea_plan_ops(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_t workers_per_gpu,

@@ -182,17 +182,9 @@ dsea_status run_plan(dsea_grid* c, int64_t n_steps)
         c->stats.hop_bytes += (int64_t)sb * n;
         return DSEA_OK;
     };
-    // Pushes must leave in (super-cycle, slot) order (the counters above).  In the
-    // stage where the last worker starts passing a trailing partial super-cycle
-    // through, the plan lists PASS(block 0 of cycle K) before BIN(last slice of cycle
-    // K-1); that BIN only pushes data computed in an earlier stage, so it is run first.
+    // pushes must leave in (super-cycle, slot) order for the counters (order_pushes)
     std::vector<Op> ops = P.ops;
-    for (size_t i = 0; i + 1 < ops.size(); i++)
-        if (ops[i].kind == OP_PASS && ops[i].worker == W - 1)
-            for (size_t k = i + 1; k < ops.size() && ops[k].stage == ops[i].stage && ops[k].worker == ops[i].worker &&
-                                   ops[k].kind == OP_BIN;
-                 k++)
-                if (ops[k].cycle < ops[i].cycle) std::rotate(ops.begin() + i, ops.begin() + k, ops.begin() + k + 1), i++;
+    order_pushes(ops, W);
     for (const Op& op : ops) {
         switch (op.kind) {
         case OP_RECV:

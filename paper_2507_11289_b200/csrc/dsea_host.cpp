@@ -270,6 +270,16 @@ Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps, const Blocks& 
 // data worker 0 waits for from the ring then depends on exactly those trailing
 // blocks, and the stream order would deadlock.  There the ring is at its plateau
 // anyway: a gap of d (W-1) stages lets every rank finish K first.
+void order_pushes(std::vector<Op>& ops, int W)
+{
+    for (size_t i = 0; i + 1 < ops.size(); i++)
+        if (ops[i].kind == OP_PASS && ops[i].worker == W - 1)
+            for (size_t k = i + 1; k < ops.size() && ops[k].stage == ops[i].stage && ops[k].worker == ops[i].worker &&
+                                   ops[k].kind == OP_BIN;
+                 k++)
+                if (ops[k].cycle < ops[i].cycle) std::rotate(ops.begin() + i, ops.begin() + k, ops.begin() + k + 1), i++;
+}
+
 bool plan_plateau(int ng, int W, const Blocks& bl)
 {
     if (ng == 1) return false;
@@ -750,17 +760,9 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             return fail(c, DSEA_EPEER, "cuStreamWriteValue32 (release) failed");
         return DSEA_OK;
     };
-    // counter mode: pushes must leave in (super-cycle, slot) order -- where the plan
-    // lists PASS(block 0 of cycle K) before BIN(last slice of K-1) for the last worker,
-    // that BIN (data binned in an earlier stage) runs first
+    // counter mode: pushes must leave in (super-cycle, slot) order (order_pushes)
     std::vector<Op> ops = P.ops;
-    if (c->ctr)
-        for (size_t i = 0; i + 1 < ops.size(); i++)
-            if (ops[i].kind == OP_PASS && ops[i].worker == W - 1)
-                for (size_t k = i + 1; k < ops.size() && ops[k].stage == ops[i].stage &&
-                                       ops[k].worker == ops[i].worker && ops[k].kind == OP_BIN;
-                     k++)
-                    if (ops[k].cycle < ops[i].cycle) std::rotate(ops.begin() + i, ops.begin() + k, ops.begin() + k + 1), i++;
+    if (c->ctr) order_pushes(ops, W);
     const size_t nops = ops.size();
     for (size_t oi = 0; oi < nops; oi++) {
         const Op& op = ops[oi];
@@ -1655,7 +1657,8 @@ dsea_status dsea_plan_ops(int32_t n_slices, int32_t n_gpus, int32_t rank, int32_
     if (!n_rows || n_slices < 1 || n_gpus < 1 || rank < 0 || rank >= n_gpus || W < 1 || n_steps < 0 ||
         slices_per_stage < 1 || slices_per_stage > n_slices)
         return DSEA_EINVAL;
-    const Plan P = build_plan(n_slices, n_gpus, rank, W, n_steps, make_blocks(n_slices, n_gpus, slices_per_stage));
+    Plan P = build_plan(n_slices, n_gpus, rank, W, n_steps, make_blocks(n_slices, n_gpus, slices_per_stage));
+    order_pushes(P.ops, W);   // as executed with the default copy-engine hop
     *n_rows = (int64_t)P.ops.size();
     if (!rows) return DSEA_OK;
     const int64_t n = std::min<int64_t>(cap_rows, (int64_t)P.ops.size());

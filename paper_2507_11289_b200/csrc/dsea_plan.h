@@ -42,6 +42,13 @@ bool plan_plateau(int ng, int W, const Blocks& bl);
 int plan_gap(int ng, int W, const Blocks& bl);
 Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps, const Blocks& bl);
 
+// Pushes to the ring successor (the last worker's BIN and PASS ops) must leave in
+// (super-cycle, slot) order for the monotone arrival/release counters.  The plan lists
+// PASS(block 0 of cycle K) before BIN(last slice of cycle K-1) in the stage where the
+// last worker starts passing a trailing partial super-cycle through; that BIN only
+// pushes data finalised in an earlier stage, so it is moved first.  In place.
+void order_pushes(std::vector<Op>& ops, int W);
+
 // stream memory operations (cuStreamWaitValue32 >= / cuStreamWriteValue32 through
 // the runtime's driver entry points): 0 on success
 int stream_wait_geq32(cudaStream_t s, const uint32_t* addr, uint32_t v);

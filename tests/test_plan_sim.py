@@ -112,3 +112,29 @@ def test_lead_blocks(ns, ng, B, lead, monkeypatch):
     assert len(rest) == -(-(ns - (4 if lead else 0)) // B)
     assert max(rest) <= B and max(rest) - min(rest) <= 1
     assert all(sz >= 2 for sz in sizes)
+
+
+def _pushes(ops, W):
+    """(cycle, slot) of every slot the last worker pushes to the ring successor, in op order."""
+    out = []
+    for kind, stage, w, j, n, K, t in (tuple(int(v) for v in o) for o in ops):
+        if w == W - 1 and kind in (BN, P):
+            out += [(K, s) for s in range(j, j + n)]
+    return out
+
+
+@pytest.mark.parametrize("ns,ng,W,B", CASES[::7] + BENCH_CASES)
+def test_pushes_leave_in_slot_order(ns, ng, W, B):
+    """What the monotone ring counters rely on (order_pushes): each rank
+    pushes every slot once per super-cycle, in strictly increasing (super-cycle, slot)
+    order -- including partial super-cycles passed through (Q15) -- and the successor's
+    receives come in the same slot order."""
+    for n_steps in (2 * ng * W, 2 * ng * W - 1, 3 * ng * W - (W > 1)):
+        plans = [D.dsea_plan_ops(ns, ng, r, W, n_steps, B) for r in range(ng)]
+        for r in range(ng):
+            p = _pushes(plans[r], W)
+            assert p == sorted(p) and len(set(p)) == len(p), (r, n_steps)
+            cycles = -(-n_steps // (ng * W))
+            assert len(p) == cycles * ns
+            recv = [int(o[3]) for o in plans[(r + 1) % ng] if int(o[0]) == R]
+            assert recv == [s for _, s in p]      # (rank 0 also takes the last cycle back, Q22)
