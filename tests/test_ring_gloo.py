@@ -307,3 +307,92 @@ def test_gloo_stencil_ring_emulation_equals_sequential(W, B, n_steps, calls):
     res = _spawn(_grid_ring_worker, 2, W, B, n_steps, calls)
     u0 = inputs.grid_field(GNX, GNY, GNZ, 3)
     assert np.array_equal(res[0], OG.run(u0, GR, n_steps))
+
+
+# ---------------------------------------------------------------- 5. MD ring emulation, general plan
+# The MD workload (O_in = O_out = 1) on two gloo ranks executing dsea_plan_ops -- blocks
+# of B slices, W workers per rank, split calls and partial super-cycles -- op by op:
+# FORCE advances each slice of the block from its neighbours (oracle pair law, _unit);
+# BIN finalises a slice from the staged contributions of slices s-1..s+1; PASS copies
+# a block through; the last worker pushes finalised slices to the successor (one
+# message per slice, in the order dsea_plan_ops returns).  Equals the whole-domain
+# oracle run.
+def _md_plan_worker(rank, world, W, B, n_steps, calls):
+    g, x, v = _initial()
+    ns = NS
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+    inb = {}
+    if rank == 0:
+        sl = _slice_of(x, g)
+        ids = np.arange(len(x))
+        for j in range(ns):
+            sel = sl == j
+            inb[j] = _pack(np.column_stack([ids[sel], x[sel], v[sel], np.zeros((sel.sum(), 3))]))
+    out = [dict() for _ in range(W)]
+    staged = [dict() for _ in range(W)]
+    pending, queue, got, expected = [], [], {}, {}
+
+    def recv_until(slot):
+        while got.get(slot, 0) < expected.get(slot, 0):
+            s = queue.pop(0)
+            n = np.zeros(1, dtype=np.int64)
+            dist.recv(_t(n), src=prv)
+            buf = np.zeros((int(n[0]), 10))
+            if n[0]:
+                dist.recv(_t(buf), src=prv)
+            inb[s] = buf
+            got[s] = got.get(s, 0) + 1
+
+    def push(rec):
+        pending.append(dist.isend(_t(np.array([len(rec)], dtype=np.int64)), dst=nxt))
+        if len(rec):
+            pending.append(dist.isend(_t(np.ascontiguousarray(rec)), dst=nxt))
+
+    per = n_steps // calls
+    for call in range(calls):
+        steps = per if call < calls - 1 else n_steps - per * (calls - 1)
+        for kind, stage, w, j, n, K, t in (tuple(int(q) for q in o) for o in D.dsea_plan_ops(ns, world, rank, W, steps, B)):
+            if kind == R_:
+                queue.append(j)
+                expected[j] = expected.get(j, 0) + 1
+                continue
+            src = inb if w == 0 else out[w - 1]
+            if kind in (F_, P_) and w == 0:
+                recv_until(min(j + n, ns - 1) if kind == F_ else j + n - 1)
+            if kind == F_:
+                for s in range(j, j + n):
+                    staged[w][s] = _unit(g, src.get(s - 1) if s > 0 else None, src[s],
+                                         src.get(s + 1) if s < ns - 1 else None)
+            elif kind == P_:
+                for s in range(j, j + n):
+                    out[w][s] = src[s]
+                    if w == W - 1:
+                        push(src[s])
+            elif kind == BN_:
+                for s in range(j, j + n):
+                    parts = [staged[w][q][0][staged[w][q][1] == s] for q in (s - 1, s, s + 1) if q in staged[w]]
+                    rec = np.concatenate(parts)
+                    out[w][s] = rec[np.argsort(rec[:, 0], kind="stable")]
+                    if w == W - 1:
+                        push(out[w][s])
+        if rank == 0:
+            recv_until(ns - 1)
+    for h in pending:
+        h.wait()
+    if rank == 0:
+        final = np.concatenate([inb[j] for j in range(ns)])
+        return final[np.argsort(final[:, 0])]
+    return "ok"
+
+
+@pytest.mark.parametrize("W,B,n_steps,calls", [(1, 2, 4, 1), (2, 2, 6, 2), (2, 3, 5, 1), (1, 3, 3, 2)])
+def test_gloo_md_plan_emulation_equals_sequential(W, B, n_steps, calls):
+    res = _spawn(_md_plan_worker, 2, W, B, n_steps, calls)
+    final = res[0]
+    g, x, v = _initial()
+    xo, vo, Fo, _ = oracle.run(x, v, np.zeros_like(x), g.b, RC, DT, n_steps)
+    assert np.array_equal(final[:, 0], np.arange(len(x)))
+    d = final[:, 1:4] - xo
+    d[:, 1:] -= g.b[1:] * np.round(d[:, 1:] / g.b[1:])
+    assert np.max(np.abs(d)) < 1e-12
+    assert np.max(np.abs(final[:, 4:7] - vo)) < 1e-11
