@@ -232,7 +232,7 @@ dsea_status dsea_set_state(dsea_ctx *ctx, const double *xyz, const double *vxyz,
  * atoms (lambda = 1 for an empty or motionless slice), v <- lambda_j v, then the
  * position update.  Per slice, so the ring needs no extra exchange.  Energies keep
  * the post-kick (pre-scale) KE.  DSEA_EINVAL if enable and T_target <= 0 or not
- * finite; DSEA_ESTATE before dsea_slice or with the non-default DSEA_FORCE_V2 kernel.
+ * finite; DSEA_ESTATE before dsea_slice.
  * Applies from the next dsea_step; on a ring every rank must set the same value. */
 dsea_status dsea_set_thermostat(dsea_ctx *ctx, int32_t enable, double T_target);
 

@@ -19,9 +19,9 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES_CU = ["dsea_kernels.cu", "dsea_grid_kernels.cu"]
+SOURCES_CU = ["dsea_kernels.cu", "dsea_force.cu", "dsea_grid_kernels.cu"]
 SOURCES_CPP = ["dsea_host.cpp", "dsea_grid.cpp"]
-HEADERS = ["dsea_internal.h", "dsea_plan.h", os.path.join("..", "..", "include", "dsea.h"),
+HEADERS = ["dsea_internal.h", "dsea_device.cuh", "dsea_plan.h", os.path.join("..", "..", "include", "dsea.h"),
            os.path.join("..", "..", "include", "dsea_grid.h")]
 
 

@@ -326,8 +326,6 @@ struct dsea_ctx {
     std::vector<void*> dallocs;
     UnitEnergy* e_dev = nullptr;
     size_t e_cap = 0;
-    double4* partials = nullptr;
-    unsigned* tickets = nullptr;
     DevErr* err_dev = nullptr;
     unsigned long long* tile_ctr = nullptr;
     double* aos_dev = nullptr;            // [3 * 3N] by-id AoS scratch for set_state / get_*
@@ -612,7 +610,7 @@ dsea_status alloc_stg(dsea_ctx* c, StgView* S)
     if ((s = dalloc(c, &S->id, n))) return s;
     if ((s = dalloc(c, &S->key, n))) return s;
     if ((s = dalloc(c, &S->n, (size_t)c->g.ns))) return s;
-    if ((s = dalloc(c, &S->eatom, n))) return s;
+    if ((s = dalloc(c, &S->eatom, energy_records(c->g, c->T)))) return s;
     CUDA_TRY(c, cudaMemset(S->key, 0, sizeof(int32_t) * n));
     CUDA_TRY(c, cudaMemset(S->n, 0, sizeof(int32_t) * (size_t)c->g.ns));
     return DSEA_OK;
@@ -806,7 +804,7 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             // reduced before the pass rewrites them (other blocks' reductions may still
             // run: they overlap this pass instead of stalling it)
             cudaEvent_t& ev_e = c->ev_energy[(size_t)w * c->bl.n() + c->bl.of[j]];
-            if (c->T.pipe) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, ev_e, 0));
+            CUDA_TRY(c, cudaStreamWaitEvent(c->cs, ev_e, 0));
             if (c->peer && !c->ce_hop && w == W - 1) {
                 // staging of this block and the arrival counters it adds to were last read
                 // by the remote bin runs of blocks c and c+1 one super-cycle ago
@@ -814,20 +812,19 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             }
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
             c->stats.kernel_launches +=
-                force_launch(c->g, c->T, in_of(w), c->stg[w], c->outb[w].cnt, j, n,
-                             c->e_dev + (size_t)op.t_rel * ns, c->partials, c->tickets, c->err_dev, c->cs);
+                force_launch(c->g, c->T, in_of(w), c->stg[w], c->outb[w].cnt, j, n, c->err_dev, c->cs);
             c->stats.force_launches++;
             if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_FORCE, {t0, t1}}); }
-            if (c->T.pipe && c->g.thermo) {  // NVT: lambda_j on the critical path, then the drift
+            if (c->g.thermo) {  // NVT: lambda_j on the critical path, then the drift
                 UnitEnergy* eo = c->e_dev + (size_t)op.t_rel * ns;
-                energy_launch(c->g, c->stg[w], j, n, eo, c->cs);
+                energy_launch(c->g, c->T, c->stg[w], j, n, eo, c->cs);
                 drift_launch(c->g, c->stg[w], j, n, eo, c->outb[w].cnt, c->err_dev, c->cs);
                 CUDA_TRY(c, cudaEventRecord(ev_e, c->cs));
                 c->stats.kernel_launches += 2;
-            } else if (c->T.pipe) {  // per-slice energy reduction off the critical path
+            } else {  // per-slice energy reduction off the critical path
                 CUDA_TRY(c, cudaEventRecord(c->ev_force[w], c->cs));
                 CUDA_TRY(c, cudaStreamWaitEvent(c->es, c->ev_force[w], 0));
-                energy_launch(c->g, c->stg[w], j, n, c->e_dev + (size_t)op.t_rel * ns, c->es);
+                energy_launch(c->g, c->T, c->stg[w], j, n, c->e_dev + (size_t)op.t_rel * ns, c->es);
                 CUDA_TRY(c, cudaEventRecord(ev_e, c->es));
                 c->stats.kernel_launches++;
             }
@@ -1068,19 +1065,18 @@ dsea_status run_fused(dsea_ctx* c, int64_t n_steps)
     for (int64_t t = 0; t < n_steps; t++) {
         cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr;
         if (c->timing) { t0 = tev(c); t1 = tev(c); t2 = tev(c); cudaEventRecord(t0, c->cs); }
-        if (c->T.pipe) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_energy[0], 0));
-        int nl = force_launch(c->g, c->T, c->inb, c->stg[0], c->inb.cnt, 0, ns,
-                              c->e_dev + (size_t)t * ns, c->partials, c->tickets, c->err_dev, c->cs);
-        if (c->T.pipe && c->g.thermo) {  // NVT: lambda_j, then the drift
+        CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_energy[0], 0));
+        int nl = force_launch(c->g, c->T, c->inb, c->stg[0], c->inb.cnt, 0, ns, c->err_dev, c->cs);
+        if (c->g.thermo) {  // NVT: lambda_j, then the drift
             UnitEnergy* eo = c->e_dev + (size_t)t * ns;
-            energy_launch(c->g, c->stg[0], 0, ns, eo, c->cs);
+            energy_launch(c->g, c->T, c->stg[0], 0, ns, eo, c->cs);
             drift_launch(c->g, c->stg[0], 0, ns, eo, c->inb.cnt, c->err_dev, c->cs);
             CUDA_TRY(c, cudaEventRecord(c->ev_energy[0], c->cs));
             nl += 2;
-        } else if (c->T.pipe) {
+        } else {
             CUDA_TRY(c, cudaEventRecord(c->ev_force[0], c->cs));
             CUDA_TRY(c, cudaStreamWaitEvent(c->es, c->ev_force[0], 0));
-            energy_launch(c->g, c->stg[0], 0, ns, c->e_dev + (size_t)t * ns, c->es);
+            energy_launch(c->g, c->T, c->stg[0], 0, ns, c->e_dev + (size_t)t * ns, c->es);
             CUDA_TRY(c, cudaEventRecord(c->ev_energy[0], c->es));
             nl++;
         }
@@ -1269,9 +1265,6 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     c->stg.resize(c->W);
     for (int w = 0; w < c->W; w++)
         if ((s = alloc_stg(c, &c->stg[w]))) return s;
-    if ((s = dalloc(c, &c->partials, (size_t)g.ns * c->T.tiles))) return s;
-    if ((s = dalloc(c, &c->tickets, (size_t)g.ns))) return s;
-    CUDA_TRY(c, cudaMemset(c->tickets, 0, sizeof(unsigned) * g.ns));
     if ((s = dalloc(c, &c->err_dev, 1))) return s;
     if ((s = dalloc(c, &c->tile_ctr, 1))) return s;
     if ((s = dalloc(c, &c->arr_dev, (size_t)g.ns))) return s;
@@ -1582,7 +1575,6 @@ dsea_status dsea_set_thermostat(dsea_ctx* c, int32_t enable, double T_target)
     if (enable && !(std::isfinite(T_target) && T_target > 0.0))
         return fail(c, DSEA_EINVAL, "thermostat temperature must be > 0 (got %g)", T_target);
     if (!c->sliced) return fail(c, DSEA_ESTATE, "dsea_set_thermostat before dsea_slice");
-    if (enable && !c->T.pipe) return fail(c, DSEA_ESTATE, "the thermostat needs the default force kernel");
     c->g.thermo = enable ? 1 : 0;
     c->g.T_target = enable ? T_target : 0.0;
     return DSEA_OK;

@@ -80,21 +80,26 @@ struct StgView {
     double *x, *y, *z, *vx, *vy, *vz, *fx, *fy, *fz;
     int32_t *id, *key;
     int32_t* n;      // [ns] atoms staged per slice
-    double4* eatom;  // [ns*cap] per-atom (u_core, vir2, ke2, pairs) of the last force pass
+    double4* eatom;  // energy records (u_core, vir2, ke2, pairs) of the last force pass:
+                     // FORCE_TILE one per tile [ns*tiles], FORCE_PIPE one per atom [ns*cap]
 };
 
-// Force-kernel tiling (one CTA = one (cx_local, cy) column x tz cells of z).
+// Force-kernel tiling.  A tile is a run of consecutive (z-sorted) home atoms of one
+// (cx_local, cy) column; tiles per slice = c * cells[1] * nzt.
+enum { FORCE_TILE = 0, FORCE_PIPE = 1 };
 struct Tiling {
-    int tz;          // home cells per z-tile
-    int nzt;         // z-tiles per column
+    int kind;        // FORCE_TILE (k_force_tile, default) or FORCE_PIPE (k_force_pipe, A/B)
+    int home;        // home atoms per tile (the column's last tile takes any remainder)
+    int nzt;         // tiles per column
     int tiles;       // tiles per slice = c * cells[1] * nzt
     int smax;        // staged atoms capacity of one CTA
-    int jpar;        // candidate parity groups (lanes = 32/jpar atoms x jpar)
-    int maxh;        // per-lane hit-list capacity
+    int maxh;        // per-lane hit-list capacity (rows)
     size_t smem;     // dynamic shared memory bytes
-    bool pipe;       // persistent pipelined kernel (default) or the one-tile-per-CTA kernel
-    int grid;        // persistent grid = SMs x resident CTAs per SM
-    unsigned long long* ctr;       // device: dynamic tile counter of this context
+    int off_hl, off_sp, off_q;     // FORCE_TILE: byte offsets of the hit lists, FP64 staging
+                                   // and FP32 screening records in dynamic shared memory
+    int grid;        // persistent grid (FORCE_PIPE) = SMs x resident CTAs per SM
+    int per_sm;      // resident CTAs per SM
+    unsigned long long* ctr;       // device: dynamic tile counter of this context (FORCE_PIPE)
     unsigned long long* ctr_base;  // host: counter value at the next launch
 };
 
@@ -116,16 +121,23 @@ struct DevErr {
     int32_t aux;
 };
 
-// ---- kernel launchers (dsea_kernels.cu) ----------------------------------
-size_t pipe_smem_bytes(int smax, int maxh);
+// ---- kernel launchers (dsea_kernels.cu, dsea_force.cu) ----------------------
+Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin);
+int force_kernel_attr(const Tiling& T);     // resident CTAs per SM (< 1: cannot launch)
 int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t* out_cnt,
-                 int j0, int nj, UnitEnergy* e_out, double4* partials, unsigned* tickets,
+                 int j0, int nj, DevErr* err, cudaStream_t s);
+size_t energy_records(const Geo& g, const Tiling& T);   // records of stg.eatom
+void energy_launch(const Geo& g, const Tiling& T, StgView stg, int j0, int nj, UnitEnergy* e_out,
+                   cudaStream_t s);
+// the pipelined kernel (A/B: DSEA_FORCE=pipe)
+Tiling pipe_tiling(const Geo& g, double mean_per_cell, int smem_optin);
+int pipe_kernel_attr(const Tiling& T);
+void pipe_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t* out_cnt, int j0, int nj,
                  DevErr* err, cudaStream_t s);
 void aos_to_stage_launch(StgView S, const double* xyz, const double* v, const double* f, int n, cudaStream_t s);
 void slots_to_aos_launch(const Geo& g, BufView in, int which, double* out, unsigned long long* count,
                          cudaStream_t s);
 void signal_launch(uint32_t* flags, int first, int n, uint32_t value, cudaStream_t s);
-void energy_launch(const Geo& g, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s);
 // NVT only: v <- lambda_j v, then the drift/walls/destination of md_v3b for the
 // staged atoms of slices [j0, j0+nj) (lambda_j from e_out[j], written by k_energy)
 void drift_launch(const Geo& g, StgView stg, int j0, int nj, const UnitEnergy* e_out, int32_t* out_cnt,
@@ -137,7 +149,5 @@ void bin_gather_launch(const Geo& g, BufView out, StgView stg, int m0, int nm, D
                        cudaStream_t s);
 void init_keys_launch(const Geo& g, StgView stg, int n, int32_t* out_cnt, DevErr* err,
                       cudaStream_t s);
-Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin);
-int force_kernel_attr(const Tiling& T);
 
 }  // namespace dsea

@@ -24,480 +24,9 @@
 #include "dsea_internal.h"
 #include "../../include/dsea.h"
 
+#include "dsea_device.cuh"
+
 namespace dsea {
-
-#define FULLMASK 0xffffffffu
-
-// Programmatic dependent launch (PDL): kernels of the compute-stream chain (force ->
-// bin scan -> place -> gather -> next force) are launched with programmatic stream
-// serialisation, so a launch and its CTAs' prologue overlap the predecessor's tail.
-// pdl_wait() blocks until the predecessor grid has completed and its memory is
-// visible (a no-op without PDL); pdl_release() lets the successor launch early.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
-__device__ __forceinline__ void set_err(DevErr* e, int code, int slice, int atom, int aux) {
-    if (atomicCAS(&e->code, 0, code) == 0) {
-        e->slice = slice;
-        e->atom = atom;
-        e->aux = aux;
-    }
-}
-
-__device__ __forceinline__ const int32_t* slot_cs(const BufView& B, int j) {
-    return reinterpret_cast<const int32_t*>(B.base + (size_t)j * B.L.slot_bytes);
-}
-__device__ __forceinline__ int32_t* slot_cs_w(const BufView& B, int j) {
-    return reinterpret_cast<int32_t*>(B.base + (size_t)j * B.L.slot_bytes);
-}
-__device__ __forceinline__ double* slot_d(const BufView& B, int j, size_t off) {
-    return reinterpret_cast<double*>(B.base + (size_t)j * B.L.slot_bytes + off);
-}
-__device__ __forceinline__ int32_t* slot_i(const BufView& B, int j, size_t off) {
-    return reinterpret_cast<int32_t*>(B.base + (size_t)j * B.L.slot_bytes + off);
-}
-
-// 1/x in FP64: MUFU approximation + Newton steps.  One step (default) leaves a relative
-// error of ~2^-45 in 1/r^2 -- about 1e-13 in a pair force, far inside the 1e-10 parity
-// bound (Q13) -- and shortens each hit's dependent FP64 chain by two DFMAs (C4 force
-// launch 10.09 -> 9.93 ms); -DDSEA_RCP_NEWTON=2 restores the correctly-rounded-like
-// reciprocal.
-#ifndef DSEA_RCP_NEWTON
-#define DSEA_RCP_NEWTON 1
-#endif
-
-__device__ __forceinline__ double rcp64(double x) {
-    double y;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double e = fma(-x, y, 1.0);
-    y = fma(y, e, y);
-#if DSEA_RCP_NEWTON >= 2
-    e = fma(-x, y, 1.0);
-    y = fma(y, e, y);
-#endif
-    return y;
-}
-
-__device__ __forceinline__ int cell_coord(double r, double l, int n) {
-    // cell = clamp(floor(r / l), 0, n-1) with IEEE division (reading Q4)
-    double q = floor(r / l);
-    if (!(q >= 0.0)) return 0;
-    if (q >= (double)(n - 1)) return n - 1;
-    return (int)q;
-}
-
-// ------------------------------------------------------------------------------
-// Force kernel.  One CTA = HOME_ATOMS consecutive (z-sorted) atoms of column (cxl, cy)
-// of slice j.  Stages the 9 neighbour columns over every cell within rc of them
-// (periodic images in y and z
-// pre-shifted; walls in x: absent columns) into shared memory, z-sorted, as FP64
-// (exact) and FP32 (screen) copies.  Every column run starts at an even index and
-// is padded to even length with a far-away dummy, so candidates are screened two
-// at a time with packed FP32x2 arithmetic.  Warps take chunks of IL = 32/JPAR
-// consecutive home atoms (dynamically, from a shared counter); lane (il, par)
-// screens every JPAR-th candidate pair of the chunk's z-window in each column
-// (shared-memory broadcast within a lane group), appends survivors to its own hit
-// list and evaluates them exactly in FP64.
-// ------------------------------------------------------------------------------
-constexpr int FORCE_THREADS = 128;
-constexpr int FORCE_WARPS = FORCE_THREADS / 32;
-constexpr int HOME_ATOMS = FORCE_WARPS * 16;   // home atoms per CTA: one 16-atom chunk per warp
-
-__device__ __forceinline__ int stage_pad(int n) { return n + (n & 1); }
-
-template <int JPAR>
-__global__ void __launch_bounds__(FORCE_THREADS)
-k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt, int j0,
-        UnitEnergy* __restrict__ e_out, double4* __restrict__ partials,
-        unsigned* __restrict__ tickets, DevErr* __restrict__ err)
-{
-    constexpr int IL = 32 / JPAR;
-    extern __shared__ __align__(16) unsigned char smem[];
-    double* sx = reinterpret_cast<double*>(smem);
-    double* sy = sx + T.smax;
-    double* sz = sy + T.smax;
-    float* fx32 = reinterpret_cast<float*>(sz + T.smax);
-    float* fy32 = fx32 + T.smax;
-    float* fz32 = fy32 + T.smax;
-    double4* chunk_e = reinterpret_cast<double4*>(fz32 + T.smax);   // [T.smax / 16 + 65]
-    uint16_t* hl = reinterpret_cast<uint16_t*>(chunk_e + (T.smax / 16 + 65));
-
-    __shared__ int p_cnt[27], p_dst[27];
-    __shared__ const double* p_src[27][3];
-    __shared__ double p_dy[27], p_dz[27];
-    __shared__ int c_lo[9], c_hi[9];
-    __shared__ int s_total, s_home_first, s_nhome, s_self_base, s_next_chunk;
-    __shared__ double s_red[FORCE_WARPS][4];
-    __shared__ bool s_last;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int j = j0 + blockIdx.y;
-    const int tile = blockIdx.x;
-    const int CY = g.cells[1], CZ = g.cells[2];
-    const int tt = tile % T.nzt;                 // tile of HOME_ATOMS atoms within the column
-    const int rest = tile / T.nzt;
-    const int cyi = rest % CY;
-    const int cxl = rest / CY;
-
-    // home atoms: [h0, h1) of column (cxl, cyi) -- a fixed atom count per CTA so that
-    // every warp gets one chunk (the last tile of a column takes any remainder)
-    const int32_t* csj = slot_cs(in, j);
-    const int colbase_h = (cxl * CY + cyi) * CZ;
-    const int col_first = csj[colbase_h], col_end = csj[colbase_h + CZ];
-    const int h0 = col_first + tt * HOME_ATOMS;
-    const int h1 = (tt == T.nzt - 1) ? col_end : min(col_end, h0 + HOME_ATOMS);
-    const double* zj = slot_d(in, j, in.L.off_z);
-    const double ox = (double)(j * g.c + cxl) * g.l[0];
-    const double oy = (double)cyi * g.l[1];
-    if (tid == 0 && tile == 0) stg.n[j] = slot_cs(in, j)[g.ncell];
-
-    int chunk_base = 0;
-    const int chunk_cap = T.smax / 16 + 64;
-    // sub-tiles: the home range is halved until its staged neighbourhood fits in
-    // shared memory (dense fluctuations never fail, they only cost an extra pass)
-    int hb = h0;
-    while (hb < h1) {
-        int he = h1;
-        double oz = 0.0;
-        for (;;) {
-            const double zfirst = zj[hb];
-            const double zlast = zj[he - 1];
-            oz = zfirst;
-            // staged z cells (inclusive): every cell within rc of a home atom; -1/CZ are images
-            const int z0 = (int)floor((zfirst - g.rc - 1e-9) / g.l[2]);
-            const int z1 = (int)floor((zlast + g.rc + 1e-9) / g.l[2]);
-    // ---- piece table: 9 columns x {low wrap, main, high wrap} -------------------
-        if (warp == 0) {
-            int cnt = 0, src_slice = 0, start = 0;
-            double dyv = 0.0, dzv = 0.0;
-            int home_first = 0, home_end = 0, main_start = 0;
-            if (lane < 27) {
-                const int col = lane / 3, q = lane % 3;
-                const int dxk = col / 3 - 1, dyk = col % 3 - 1;
-                const int gx = j * g.c + cxl + dxk;
-                if (gx >= 0 && gx < g.cells[0]) {
-                    const int m = gx / g.c, cx2 = gx - m * g.c;
-                    int cyy = cyi + dyk;
-                    if (cyy < 0) { cyy += CY; dyv = -g.b[1]; }
-                    else if (cyy >= CY) { cyy -= CY; dyv = g.b[1]; }
-                    const int zlo = max(z0, -1), zhi = min(z1, CZ);  // inclusive
-                    int a = 0, b = -1;
-                    if (q == 0) { if (zlo < 0) { a = zlo + CZ; b = CZ - 1; dzv = -g.b[2]; } }
-                    else if (q == 1) { a = max(zlo, 0); b = min(zhi, CZ - 1); }
-                    else { if (zhi >= CZ) { a = 0; b = zhi - CZ; dzv = g.b[2]; } }
-                    if (b >= a) {
-                        const int32_t* cs = slot_cs(in, m);
-                        const int colbase = (cx2 * CY + cyy) * CZ;
-                        start = cs[colbase + a];
-                        cnt = cs[colbase + b + 1] - start;
-                        src_slice = m;
-                        if (col == 4 && q == 1) {
-                            home_first = hb;
-                            home_end = he;
-                            main_start = start;
-                        }
-                    }
-                }
-            }
-            // column totals -> the last piece of each column carries the even padding
-            const int grp = lane - lane % 3;
-            int coltot = __shfl_sync(FULLMASK, cnt, grp) + __shfl_sync(FULLMASK, cnt, min(grp + 1, 31)) +
-                         __shfl_sync(FULLMASK, cnt, min(grp + 2, 31));
-            const int span = cnt + ((lane < 27 && lane % 3 == 2) ? (coltot & 1) : 0);
-            int incl = span;
-    #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int v = __shfl_up_sync(FULLMASK, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const int excl = incl - span;
-            if (lane < 27) {
-                p_cnt[lane] = cnt;
-                p_dst[lane] = excl; p_dy[lane] = dyv; p_dz[lane] = dzv;
-                p_src[lane][0] = slot_d(in, src_slice, in.L.off_x) + start;
-                p_src[lane][1] = slot_d(in, src_slice, in.L.off_y) + start;
-                p_src[lane][2] = slot_d(in, src_slice, in.L.off_z) + start;
-            }
-            if (lane == 31) s_total = incl;
-            if (lane == 13) {
-                s_home_first = home_first;
-                s_nhome = home_end - home_first;
-                s_self_base = excl + (home_first - main_start);
-            }
-            if (lane == 0) s_next_chunk = FORCE_WARPS;
-        }
-            __syncthreads();
-            if (s_total <= T.smax) break;
-            if (he - hb <= 16) {
-                if (tid == 0) set_err(err, DSEA_ECAPACITY, j, -1, s_total);
-                return;
-            }
-            he = hb + (((he - hb) / 2 + 15) & ~15);
-            __syncthreads();
-        }
-        if (tid < 9) {
-            const int lo = p_dst[3 * tid];
-            const int hi = p_dst[3 * tid + 2] + p_cnt[3 * tid + 2];
-            c_lo[tid] = lo;
-            c_hi[tid] = hi;
-            if ((hi - lo) & 1) {  // dummy far away: never passes the FP32 screen
-                fx32[hi] = 1e30f; fy32[hi] = 1e30f; fz32[hi] = 1e30f;
-                sx[hi] = 1e300; sy[hi] = 1e300; sz[hi] = 1e300;
-            }
-        }
-    // ---- stage neighbour atoms: warps take columns, lanes stride along a column -------
-        for (int col = warp; col < 9; col += FORCE_WARPS) {
-            const int n0 = p_cnt[3 * col], n1 = p_cnt[3 * col + 1], n2 = p_cnt[3 * col + 2];
-            const int dst = p_dst[3 * col];
-            const int n = n0 + n1 + n2;
-            const double* s0x = p_src[3 * col][0]; const double* s0y = p_src[3 * col][1]; const double* s0z = p_src[3 * col][2];
-            const double* s1x = p_src[3 * col + 1][0]; const double* s1y = p_src[3 * col + 1][1]; const double* s1z = p_src[3 * col + 1][2];
-            const double* s2x = p_src[3 * col + 2][0]; const double* s2y = p_src[3 * col + 2][1]; const double* s2z = p_src[3 * col + 2][2];
-            const double dy0 = p_dy[3 * col], dz0 = p_dz[3 * col], dz2 = p_dz[3 * col + 2];
-    #pragma unroll 4
-            for (int t = lane; t < n; t += 32) {
-                const bool a0 = t < n0, a1 = !a0 && t < n0 + n1;
-                const int i = a0 ? t : a1 ? t - n0 : t - n0 - n1;
-                const double* px = a0 ? s0x : a1 ? s1x : s2x;
-                const double* py = a0 ? s0y : a1 ? s1y : s2y;
-                const double* pz = a0 ? s0z : a1 ? s1z : s2z;
-                const double x = __ldg(px + i);
-                const double y = __ldg(py + i) + dy0;
-                const double z = __ldg(pz + i) + (a0 ? dz0 : a1 ? 0.0 : dz2);
-                const int d = dst + t;
-                sx[d] = x; sy[d] = y; sz[d] = z;
-                fx32[d] = (float)(x - ox); fy32[d] = (float)(y - oy); fz32[d] = (float)(z - oz);
-            }
-        }
-        __syncthreads();
-        {
-    const int nhome = s_nhome, self_base = s_self_base, home_first = s_home_first;
-            const int il = lane % IL, par = lane / IL;
-            const float rc2s = g.rc2_screen;
-            const double rc2 = g.rc2;
-            const int maxh = T.maxh;
-            const float2* X2 = reinterpret_cast<const float2*>(fx32);
-            const float2* Y2 = reinterpret_cast<const float2*>(fy32);
-            const float2* Z2 = reinterpret_cast<const float2*>(fz32);
-            constexpr int SEG_PAIRS = 32;                       // candidate pairs per segment
-            constexpr int seg_need = 2 * ((SEG_PAIRS + JPAR - 1) / JPAR);  // max appends per lane
-        
-            const int nchunks = (nhome + IL - 1) / IL;
-            if (chunk_base + nchunks > chunk_cap) {
-                if (tid == 0) set_err(err, DSEA_ECAPACITY, j, -1, chunk_base + nchunks);
-                return;
-            }
-            int ch = warp;
-            while (ch < nchunks) {
-                const int q = ch * IL + il;
-                const bool valid = q < nhome;
-                const int si = self_base + (valid ? q : nhome - 1);
-                const double xi = sx[si], yi = sy[si], zi = sz[si];
-                const float xf = valid ? fx32[si] : 1e30f, yf = fy32[si], zf = fz32[si];
-                const float2 xi2 = make_float2(xf, xf), yi2 = make_float2(yf, yf), zi2 = make_float2(zf, zf);
-                const float2 m1 = make_float2(-1.f, -1.f);
-                const double zmin = sz[self_base + ch * IL];
-                const double zmax = sz[self_base + min(ch * IL + IL, nhome) - 1];
-        
-                // z-windows of the chunk in each column (binary searches in parallel)
-                int wb = 0;
-                if (lane < 9 || (lane >= 16 && lane < 25)) {
-                    const int col = lane < 9 ? lane : lane - 16;
-                    int lo = c_lo[col], hi = c_hi[col];
-                    const int base = lo;
-                    if (lane < 9) {
-                        const double key = zmin - g.rc - 1e-9;
-                        while (lo < hi) { int mid = (lo + hi) >> 1; if (sz[mid] < key) lo = mid + 1; else hi = mid; }
-                        wb = base + ((lo - base) & ~1);                // round down to the pair start
-                    } else {
-                        const double key = zmax + g.rc + 1e-9;
-                        while (lo < hi) { int mid = (lo + hi) >> 1; if (sz[mid] <= key) lo = mid + 1; else hi = mid; }
-                        wb = base + ((lo - base + 1) & ~1);            // round up (may take the dummy)
-                    }
-                }
-        
-                double fx = 0.0, fy = 0.0, fz = 0.0;
-                double e_u = 0.0, e_v = 0.0, e_ke = 0.0;
-                int e_np = 0;
-                int cnt = 0;
-                uint16_t* hp = hl + tid;
-        
-                auto flush = [&]() {
-                    for (int m = 0; m < cnt; m++) {
-                        const int kk = hl[m * FORCE_THREADS + tid];
-                        const double dx = xi - sx[kk];
-                        const double dy = yi - sy[kk];
-                        const double dz = zi - sz[kk];
-                        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-                        if (r2 <= rc2 && kk != si) {  // inclusive cutoff; i != j
-                            const double s = rcp64(r2);
-                            const double s3 = s * s * s;                // r^-6
-                            const double t = fma(2.0, s3, -1.0);        // 2 r^-6 - 1
-                            const double gq = s3 * t;                   // 2 r^-12 - r^-6
-                            const double f = s * gq;                    // F_abs / 24
-                            fx = fma(dx, f, fx);
-                            fy = fma(dy, f, fy);
-                            fz = fma(dz, f, fz);
-                            e_u += fma(s3, s3, -s3);                    // r^-12 - r^-6
-                            e_v += gq;                                  // 2 r^-12 - r^-6
-                            e_np += 1;
-                        }
-                    }
-                    cnt = 0;
-                    hp = hl + tid;
-                };
-        
-        #pragma unroll 1
-                for (int col = 0; col < 9; col++) {
-                    const int plo = __shfl_sync(FULLMASK, wb, col) >> 1;
-                    const int phi = __shfl_sync(FULLMASK, wb, 16 + col) >> 1;
-                    for (int s0 = plo; s0 < phi; s0 += SEG_PAIRS) {
-                        const int e = min(phi, s0 + SEG_PAIRS);
-                        cnt = (int)(hp - (hl + tid)) / FORCE_THREADS;
-                        if (__any_sync(FULLMASK, cnt + seg_need > maxh)) flush();
-        #pragma unroll 4
-                        for (int m = s0 + par; m < e; m += JPAR) {
-                            const float2 X = X2[m], Y = Y2[m], Z = Z2[m];
-                            const float2 dx = __ffma2_rn(X, m1, xi2);
-                            const float2 dy = __ffma2_rn(Y, m1, yi2);
-                            const float2 dz = __ffma2_rn(Z, m1, zi2);
-                            float2 r2 = __fmul2_rn(dz, dz);
-                            r2 = __ffma2_rn(dy, dy, r2);
-                            r2 = __ffma2_rn(dx, dx, r2);
-                            const int k = 2 * m;
-                            if (r2.x <= rc2s) { *hp = (uint16_t)k; hp += FORCE_THREADS; }
-                            if (r2.y <= rc2s) { *hp = (uint16_t)(k + 1); hp += FORCE_THREADS; }
-                        }
-                    }
-                }
-                cnt = (int)(hp - (hl + tid)) / FORCE_THREADS;
-                flush();
-        
-                // combine the JPAR partial forces of each home atom (fixed xor tree)
-        #pragma unroll
-                for (int o = IL; o < 32; o <<= 1) {
-                    fx += __shfl_xor_sync(FULLMASK, fx, o);
-                    fy += __shfl_xor_sync(FULLMASK, fy, o);
-                    fz += __shfl_xor_sync(FULLMASK, fz, o);
-                }
-        
-                if (valid && par == 0) {
-                    // Algorithm 1: velocity update and position update
-                    const int gi = home_first + q;
-                    const double Fx = 24.0 * fx, Fy = 24.0 * fy, Fz = 24.0 * fz;
-                    const double fxo = slot_d(in, j, in.L.off_fx)[gi];
-                    const double fyo = slot_d(in, j, in.L.off_fy)[gi];
-                    const double fzo = slot_d(in, j, in.L.off_fz)[gi];
-                    double vx = slot_d(in, j, in.L.off_vx)[gi];
-                    double vy = slot_d(in, j, in.L.off_vy)[gi];
-                    double vz = slot_d(in, j, in.L.off_vz)[gi];
-                    const int id = slot_i(in, j, in.L.off_id)[gi];
-                    const double hdt = 0.5 * g.dt;
-                    vx = vx + (Fx + fxo) * hdt;
-                    vy = vy + (Fy + fyo) * hdt;
-                    vz = vz + (Fz + fzo) * hdt;
-                    e_ke += vx * vx + vy * vy + vz * vz;
-                    const double hdt2 = 0.5 * (g.dt * g.dt);
-                    double x = xi + vx * g.dt + Fx * hdt2;
-                    double y = yi + vy * g.dt + Fy * hdt2;
-                    double z = zi + vz * g.dt + Fz * hdt2;
-                    double Fxn = Fx;
-                    // x: mirror at 0 and b_x (reading Q2: fold r, negate v_x and F_x)
-                    if (x < 0.0) { x = -x; vx = -vx; Fxn = -Fxn; }
-                    else if (x > g.b[0]) { x = 2.0 * g.b[0] - x; vx = -vx; Fxn = -Fxn; }
-                    // y, z: periodic (Q1)
-                    if (y < 0.0) y += g.b[1]; else if (y >= g.b[1]) y -= g.b[1];
-                    if (z < 0.0) z += g.b[2]; else if (z >= g.b[2]) z -= g.b[2];
-                    // destination slice and cell (migration, md_v3b P:316-318)
-                    const int cxg = cell_coord(x, g.l[0], g.cells[0]);
-                    const int cyg = cell_coord(y, g.l[1], CY);
-                    const int czg = cell_coord(z, g.l[2], CZ);
-                    const int m = cxg / g.c;
-                    if (!(isfinite(x) && isfinite(y) && isfinite(z)) || m < j - 1 || m > j + 1) {
-                        set_err(err, DSEA_EUNSTABLE, j, id, m);
-                    } else {
-                        const int key = m * g.ncell + ((cxg - m * g.c) * CY + cyg) * CZ + czg;
-                        const size_t st = (size_t)j * g.cap + gi;
-                        stg.x[st] = x; stg.y[st] = y; stg.z[st] = z;
-                        stg.vx[st] = vx; stg.vy[st] = vy; stg.vz[st] = vz;
-                        stg.fx[st] = Fxn; stg.fy[st] = Fy; stg.fz[st] = Fz;
-                        stg.id[st] = id;
-                        stg.key[st] = key;
-                        atomicAdd(&out_cnt[key], 1);
-                    }
-                }
-                // chunk energies: fixed xor tree within the warp, stored by chunk index so the
-                // CTA total does not depend on which warp took which chunk
-                double np = (double)e_np;
-        #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    e_u += __shfl_xor_sync(FULLMASK, e_u, o);
-                    e_v += __shfl_xor_sync(FULLMASK, e_v, o);
-                    e_ke += __shfl_xor_sync(FULLMASK, e_ke, o);
-                    np += __shfl_xor_sync(FULLMASK, np, o);
-                }
-                if (lane == 0) chunk_e[chunk_base + ch] = make_double4(e_u, e_v, e_ke, np);
-                // next chunk (dynamic: warps that finish early take more)
-                int nxt = 0;
-                if (lane == 0) nxt = atomicAdd(&s_next_chunk, 1);
-                ch = __shfl_sync(FULLMASK, nxt, 0);
-            }
-        
-        }
-        __syncthreads();
-        chunk_base += (s_nhome + 15) / 16;
-        hb = he;
-    }
-    const int nchunks = chunk_base;
-
-    if (warp == 0) {
-        double a = 0, b = 0, c = 0, d = 0;
-        for (int k = lane; k < nchunks; k += 32) {
-            const double4 p = chunk_e[k];
-            a += p.x; b += p.y; c += p.z; d += p.w;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            a += __shfl_xor_sync(FULLMASK, a, o);
-            b += __shfl_xor_sync(FULLMASK, b, o);
-            c += __shfl_xor_sync(FULLMASK, c, o);
-            d += __shfl_xor_sync(FULLMASK, d, o);
-        }
-        if (lane == 0) {
-            partials[(size_t)j * T.tiles + tile] = make_double4(a, b, c, d);
-            __threadfence();
-            const unsigned t = atomicAdd(&tickets[j], 1u);
-            s_last = (t == (unsigned)(T.tiles - 1));
-        }
-    }
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        double a = 0, b = 0, c = 0, d = 0;
-        for (int k = tid; k < T.tiles; k += FORCE_THREADS) {
-            const double2* pp = reinterpret_cast<const double2*>(&partials[(size_t)j * T.tiles + k]);
-            const double2 p0 = __ldcg(pp), p1 = __ldcg(pp + 1);
-            a += p0.x; b += p0.y; c += p1.x; d += p1.y;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            a += __shfl_xor_sync(FULLMASK, a, o);
-            b += __shfl_xor_sync(FULLMASK, b, o);
-            c += __shfl_xor_sync(FULLMASK, c, o);
-            d += __shfl_xor_sync(FULLMASK, d, o);
-        }
-        if (lane == 0) { s_red[warp][0] = a; s_red[warp][1] = b; s_red[warp][2] = c; s_red[warp][3] = d; }
-        __syncthreads();
-        if (tid == 0) {
-            double A = 0, B = 0, C = 0, D = 0;
-            for (int w = 0; w < FORCE_WARPS; w++) { A += s_red[w][0]; B += s_red[w][1]; C += s_red[w][2]; D += s_red[w][3]; }
-            UnitEnergy ue;
-            ue.u_core = A; ue.vir2 = B; ue.ke2 = C; ue.npairs = D;
-            e_out[j] = ue;
-            tickets[j] = 0u;
-        }
-    }
-}
 
 // ------------------------------------------------------------------------------
 // Persistent pipelined force kernel (default).  Same arithmetic and the same
@@ -512,41 +41,6 @@ k_force(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt,
 // Energies are written per atom (u, v, ke, pairs) and reduced per slice in a fixed
 // order by k_energy, so the result does not depend on which warp took which chunk.
 // ------------------------------------------------------------------------------
-// Position update of md_v3b for one atom whose kick is done:
-// drift, mirror in x (Q2), wrap in y/z (Q1), destination slot/cell (must be j-1, j
-// or j+1, else EUNSTABLE), staging stores and the arrival count of the cell.
-__device__ __forceinline__ void drift_store(const Geo& g, const StgView& stg, size_t st, int j, double xi,
-                                            double yi, double zi, double vx, double vy, double vz, double Fx,
-                                            double Fy, double Fz, int id, int32_t* __restrict__ out_cnt,
-                                            DevErr* __restrict__ err)
-{
-    const int CY = g.cells[1], CZ = g.cells[2];
-    const double hdt2 = 0.5 * (g.dt * g.dt);
-    double x = xi + vx * g.dt + Fx * hdt2;
-    double y = yi + vy * g.dt + Fy * hdt2;
-    double z = zi + vz * g.dt + Fz * hdt2;
-    double Fxn = Fx;
-    if (x < 0.0) { x = -x; vx = -vx; Fxn = -Fxn; }                       // Q2
-    else if (x > g.b[0]) { x = 2.0 * g.b[0] - x; vx = -vx; Fxn = -Fxn; }
-    if (y < 0.0) y += g.b[1]; else if (y >= g.b[1]) y -= g.b[1];         // Q1
-    if (z < 0.0) z += g.b[2]; else if (z >= g.b[2]) z -= g.b[2];
-    const int cxg = cell_coord(x, g.l[0], g.cells[0]);
-    const int cyg = cell_coord(y, g.l[1], CY);
-    const int czg = cell_coord(z, g.l[2], CZ);
-    const int m = cxg / g.c;
-    if (!(isfinite(x) && isfinite(y) && isfinite(z)) || m < j - 1 || m > j + 1) {
-        set_err(err, DSEA_EUNSTABLE, j, id, m);
-        stg.key[st] = -1;
-    } else {
-        const int key = m * g.ncell + ((cxg - m * g.c) * CY + cyg) * CZ + czg;
-        stg.x[st] = x; stg.y[st] = y; stg.z[st] = z;
-        stg.vx[st] = vx; stg.vy[st] = vy; stg.vz[st] = vz;
-        stg.fx[st] = Fxn; stg.fy[st] = Fy; stg.fz[st] = Fz;
-        stg.id[st] = id;
-        stg.key[st] = key;
-        atomicAdd(&out_cnt[key], 1);
-    }
-}
 
 #ifndef DSEA_PIPE_CW
 #define DSEA_PIPE_CW 4
@@ -1013,15 +507,16 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
 constexpr int ENERGY_THREADS = 256;
 
 __global__ void __launch_bounds__(ENERGY_THREADS)
-k_energy(Geo g, StgView stg, int j0, UnitEnergy* __restrict__ e_out)
+k_energy(Geo g, StgView stg, int j0, int stride, int nrec, UnitEnergy* __restrict__ e_out)
 {
     pdl_wait();
     pdl_release();
     const int j = j0 + blockIdx.x;
     const int n = stg.n[j];
-    const double4* e = stg.eatom + (size_t)j * g.cap;
+    const double4* e = stg.eatom + (size_t)j * stride;
+    const int nr = nrec > 0 ? nrec : n;     // per-tile records, or one per staged atom
     double a = 0, b = 0, c = 0, d = 0;
-    for (int p = threadIdx.x; p < n; p += ENERGY_THREADS) {
+    for (int p = threadIdx.x; p < nr; p += ENERGY_THREADS) {
         const double4 v = e[p];
         a += v.x; b += v.y; c += v.z; d += v.w;
     }
@@ -1327,135 +822,64 @@ void slots_to_aos_launch(const Geo& g, BufView in, int which, double* out, unsig
 }
 
 // ------------------------------------------------------------------------------
-// Host-side launchers
+// Host-side launchers of the pipelined force kernel (A/B against k_force_tile,
+// DSEA_FORCE=pipe) and of the bin / energy / helper kernels
 // ------------------------------------------------------------------------------
-static size_t force_smem_bytes(int smax, int /*jpar*/, int maxh)
-{
-    return (size_t)smax * (3 * sizeof(double) + 3 * sizeof(float)) +
-           (size_t)(smax / 16 + 64 + 1) * sizeof(double4) + (size_t)maxh * FORCE_THREADS * sizeof(uint16_t);
-}
-
-
 static size_t pipe_smem_attr = 0;    // largest dynamic smem set on k_force_pipe so far
 
-static double env_num(const char* name, double dflt)
+Tiling pipe_tiling(const Geo& g, double mean_per_cell, int smem_optin)
 {
-    const char* v = getenv(name);
-    return (v && *v) ? atof(v) : dflt;
-}
-
-// launch with programmatic stream serialisation (DSEA_PDL=0: plain launches, A/B)
-static bool pdl_on()
-{
-    static const bool on = env_num("DSEA_PDL", 1) != 0;
-    return on;
-}
-template <typename... KArgs, typename... Args>
-static void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args)
-{
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl_on() ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
-}
-
-Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
-{
-    // defaults from the B200 measurements in profiles/; DSEA_* overrides for sweeps
     Tiling T{};
-    T.jpar = 2;
+    T.kind = FORCE_PIPE;
     T.maxh = (int)env_num("DSEA_MAXH", 64);
-    const double margin = env_num("DSEA_MARGIN", 1.25);
     const int CZ = g.cells[2];
     const double mean_col = mean_per_cell * CZ;               // atoms per column
     const double dens = mean_per_cell / g.l[2];                // atoms per sigma of column
-    // tiles per column: HOME_ATOMS atoms each, with headroom for density fluctuations
-    T.nzt = std::max(1, (int)std::ceil(1.25 * mean_col / HOME_ATOMS) + 1);
-    T.tz = 0;
-    // staged atoms: 9 columns x (home extent + 2 rc + partial cells at both ends)
-    const double per_col = std::min(mean_col + 2.0 * mean_per_cell,
-                                    HOME_ATOMS + (2.0 * g.rc + g.l[2]) * dens);
-    const double expected = 9.0 * per_col + 18.0;
-    T.smax = ((int)(margin * expected + 96.0) + 31) / 32 * 32;
-    while (T.smax > 32 && force_smem_bytes(T.smax, T.jpar, T.maxh) > (size_t)smem_optin) T.smax -= 32;
-    if (T.smax > 65534) T.smax = 65504;  // uint16 hit-list indices
-    T.smem = force_smem_bytes(T.smax, T.jpar, T.maxh);
+    T.home = PIPE_HOME;
+    T.nzt = std::max(1, (int)std::ceil(1.25 * mean_col / PIPE_HOME) + 1);
     T.tiles = g.c * g.cells[1] * T.nzt;
-    T.pipe = env_num("DSEA_FORCE_V2", 0) == 0;
-    if (T.pipe) {
-        T.jpar = 2;
-        T.nzt = std::max(1, (int)std::ceil(1.25 * mean_col / PIPE_HOME) + 1);
-        T.tiles = g.c * g.cells[1] * T.nzt;
-        const double per_col_p = std::min(mean_col + 2.0 * mean_per_cell,
-                                          PIPE_HOME + (2.0 * g.rc + g.l[2]) * dens);
-        const double expected_p = 9.0 * per_col_p + 18.0;
-        T.smax = ((int)(env_num("DSEA_PIPE_MARGIN", 1.2) * expected_p + 64.0) + 31) / 32 * 32;
-        while (T.smax > 32 && pipe_smem_bytes(T.smax, T.maxh) > (size_t)smem_optin) T.smax -= 32;
-        if (T.smax > 65504) T.smax = 65504;
-        T.smem = pipe_smem_bytes(T.smax, T.maxh);
-    }
+    const double per_col_p = std::min(mean_col + 2.0 * mean_per_cell,
+                                      PIPE_HOME + (2.0 * g.rc + g.l[2]) * dens);
+    const double expected_p = 9.0 * per_col_p + 18.0;
+    T.smax = ((int)(env_num("DSEA_PIPE_MARGIN", 1.2) * expected_p + 64.0) + 31) / 32 * 32;
+    while (T.smax > 32 && pipe_smem_bytes(T.smax, T.maxh) > (size_t)smem_optin) T.smax -= 32;
+    if (T.smax > 65504) T.smax = 65504;
+    T.smem = pipe_smem_bytes(T.smax, T.maxh);
     return T;
 }
 
-int force_kernel_attr(const Tiling& T)
+int pipe_kernel_attr(const Tiling& T)
 {
-    if (T.pipe) {
-        // the attribute is process-wide: keep the largest request of any context
-        if (T.smem > pipe_smem_attr) {
-            cudaError_t e = cudaFuncSetAttribute(k_force_pipe<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)T.smem);
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(k_force_pipe<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)T.smem);
-            if (e != cudaSuccess) return -1;
-            pipe_smem_attr = T.smem;
-        }
-        int per_sm = 0, per_sm_nvt = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force_pipe<2, false>, PIPE_THREADS, T.smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_nvt, k_force_pipe<2, true>, PIPE_THREADS, T.smem);
-        per_sm = std::min(per_sm, per_sm_nvt);   // one grid size serves both instantiations
-        if (per_sm < 1) return -1;
-        return per_sm;
+    // the attribute is process-wide: keep the largest request of any context
+    if (T.smem > pipe_smem_attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_force_pipe<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)T.smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_force_pipe<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)T.smem);
+        if (e != cudaSuccess) return -1;
+        pipe_smem_attr = T.smem;
     }
-    cudaError_t e = T.jpar == 4
-        ? cudaFuncSetAttribute(k_force<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem)
-        : cudaFuncSetAttribute(k_force<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem);
-    return e == cudaSuccess ? 0 : -1;
+    int per_sm = 0, per_sm_nvt = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force_pipe<2, false>, PIPE_THREADS, T.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_nvt, k_force_pipe<2, true>, PIPE_THREADS, T.smem);
+    return std::min(per_sm, per_sm_nvt);   // one grid size serves both instantiations
 }
 
-int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t* out_cnt, int j0,
-                 int nj, UnitEnergy* e_out, double4* partials, unsigned* tickets, DevErr* err,
-                 cudaStream_t s)
+void pipe_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t* out_cnt, int j0, int nj,
+                 DevErr* err, cudaStream_t s)
 {
-    if (T.pipe) {
-        // the tile counter is never reset: each launch consumes exactly ntiles + grid
-        // increments, so the host tracks the base of every launch
-        // NVE: force + kick + drift + destination in one pass; NVT: force + kick (the
-        // drift needs the slice's lambda, k_drift)
-        if (g.thermo)
-            launch(k_force_pipe<2, true>, T.grid, PIPE_THREADS, T.smem, s, g, T, in, stg, out_cnt, j0, nj, err,
-                   T.ctr, *T.ctr_base);
-        else
-            launch(k_force_pipe<2, false>, T.grid, PIPE_THREADS, T.smem, s, g, T, in, stg, out_cnt, j0, nj, err,
-                   T.ctr, *T.ctr_base);
-        *T.ctr_base += (unsigned long long)nj * T.tiles + T.grid;
-        return 1;
-    }
-    dim3 grid(T.tiles, nj);
-    if (T.jpar == 4)
-        k_force<4><<<grid, FORCE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, e_out, partials,
-                                                       tickets, err);
+    // the tile counter is never reset: each launch consumes exactly ntiles + grid
+    // increments, so the host tracks the base of every launch
+    // NVE: force + kick + drift + destination in one pass; NVT: force + kick (the
+    // drift needs the slice's lambda, k_drift)
+    if (g.thermo)
+        launch(k_force_pipe<2, true>, T.grid, PIPE_THREADS, T.smem, s, g, T, in, stg, out_cnt, j0, nj, err,
+               T.ctr, *T.ctr_base);
     else
-        k_force<2><<<grid, FORCE_THREADS, T.smem, s>>>(g, T, in, stg, out_cnt, j0, e_out, partials,
-                                                       tickets, err);
-    return 1;
+        launch(k_force_pipe<2, false>, T.grid, PIPE_THREADS, T.smem, s, g, T, in, stg, out_cnt, j0, nj, err,
+               T.ctr, *T.ctr_base);
+    *T.ctr_base += (unsigned long long)nj * T.tiles + T.grid;
 }
 
 // Ring-hop signal (peer backend): after the bin kernels wrote slots [first, first+n)
@@ -1478,9 +902,16 @@ void signal_launch(uint32_t* flags, int first, int n, uint32_t value, cudaStream
     launch(k_signal, 1, 64, 0, s, flags, first, n, value);
 }
 
-void energy_launch(const Geo& g, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s)
+size_t energy_records(const Geo& g, const Tiling& T)
 {
-    launch(k_energy, nj, ENERGY_THREADS, 0, s, g, stg, j0, e_out);
+    return T.kind == FORCE_PIPE ? (size_t)g.ns * g.cap : (size_t)g.ns * T.tiles;
+}
+
+void energy_launch(const Geo& g, const Tiling& T, StgView stg, int j0, int nj, UnitEnergy* e_out, cudaStream_t s)
+{
+    // records of slice j: one per tile (k_force_tile) or one per staged atom (k_force_pipe)
+    const int stride = T.kind == FORCE_PIPE ? g.cap : T.tiles;
+    launch(k_energy, nj, ENERGY_THREADS, 0, s, g, stg, j0, stride, T.kind == FORCE_PIPE ? 0 : T.tiles, e_out);
 }
 
 void drift_launch(const Geo& g, StgView stg, int j0, int nj, const UnitEnergy* e_out, int32_t* out_cnt,

@@ -1,13 +1,11 @@
 #!/bin/bash
-# iteration call: GPU tests (fast subset), perf probe, ncu of the force kernel
+# one iteration on a B200: parity tests of the single-GPU path, force-kernel timing
+# (default tile kernel vs the pipelined A/B kernel), default bench
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-mkdir -p gpurun_out
-CFG=${CFG:-C2}
-timeout 900 python -m pytest tests -m gpu -q -x -k "${PYTEST_K:-not nve}" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python scripts/prof_force.py C2 6 > gpurun_out/prof_plain.log 2>&1
-timeout 300 python scripts/prof_force.py C4 3 >> gpurun_out/prof_plain.log 2>&1
-if [ "${NCU:-1}" = "1" ]; then
-timeout 300 python scripts/prof_force.py $CFG 4 > gpurun_out/prof_plain2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_force -s 2 -c 1 -o gpurun_out/prof_force_$CFG python scripts/prof_force.py $CFG 4 > gpurun_out/ncu_full.log 2>&1
-echo "ncu rc=$?" >> gpurun_out/ncu_full.log
-fi
+O=gpurun_out/${TAG:-iter}; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_nvt.py -x -q ${PYTEST_K:+-k "$PYTEST_K"} > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log
+for c in C2 C4; do
+  timeout 300 python scripts/prof_force.py $c 6 > $O/prof_tile_$c.log 2>&1
+  DSEA_FORCE=pipe timeout 300 python scripts/prof_force.py $c 6 > $O/prof_pipe_$c.log 2>&1
+done
+timeout 600 python bench.py --steps 20 --warmup 5 > $O/bench.log 2>&1; echo "rc=$?" >> $O/bench.log
