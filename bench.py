@@ -466,7 +466,7 @@ def main():
                          "traffic": (None if traffic_pa is None else traffic_pa * atoms_per_launch),
                          "traffic_note": "dram read+write bytes per launch: ncu per-atom figure "
                                          "(profiles/r*/force_traffic.json) x atoms per launch",
-                         "kernel": "k_force_pipe (force + kick + drift + migration key; NVT: "
+                         "kernel": "k_force_tile (force + kick + drift + migration key; NVT: "
                                    "force + kick, drift in k_drift)",
                          "peak_note": f"FP64: {N_SMS} SMs x {FP64_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz",
                          "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
