@@ -1,7 +1,9 @@
-"""One rank of a multi-GPU ring check (launched by tests/test_gpu_ring.py through
-torchrun): slices stream through N_GPU processes, one GPU each, over NCCL links
-(§3.1).  Rank 0 writes the final state to an .npz for comparison with a
-single-GPU run of the same workload."""
+"""One rank of a ring check (launched by tests/test_gpu_ring.py and
+tests/test_gpu_ring_shared.py through torchrun): slices stream through N_GPU processes
+(§3.1), one GPU each -- or, with --shared-device, all on GPU 0 (gloo for the
+plumbing: NCCL refuses two ranks on one GPU; the hop itself is still the CUDA IPC map,
+copy-engine push and stream flags of the peer backend).  Rank 0 writes the final state
+to an .npz for comparison with a single-GPU run and with the oracle."""
 import argparse
 import os
 import sys
@@ -35,13 +37,20 @@ def main():
     ap.add_argument("--block", type=int, default=0, help="slices per stage (0 = auto)")
     ap.add_argument("--hop", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--thermo", type=float, default=0.0, help="NVT thermostat T (0 = NVE)")
+    ap.add_argument("--shared-device", action="store_true",
+                    help="every rank on GPU 0, gloo process group (peer hop only)")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if a.shared_device:
+        local = 0
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = CONFIGS[a.config]
     e = D.Engine(D.Box(c.nx, c.ny, c.nz, c.rho, c.rc, c.dt, c.T0, c.seed))
     e.slice(n_slices=c.n_slices, cells_per_slice_x=c.cells_per_slice_x, n_gpus=world, rank=rank,

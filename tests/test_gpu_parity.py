@@ -370,3 +370,99 @@ def test_empty_slices(mode, W, B):
     assert np.abs(d).max() <= 1e-8
     _cells_exact(e, c)
     e.close()
+
+
+def test_melted_state_parity():
+    """Reading Q13 asks for thermalised states: C1 melted for 200 steps by the ORACLE
+    (T* drops from 1.0 to ~0.55, the lattice order is gone), injected through
+    dsea_set_state with its F_new (the next kick needs F_old), then 10 GPU steps against
+    10 more oracle steps: first-step forces within 1e-10 (Q13), positions within 1e-8
+    after 10 steps (Q14), energies within 1e-10, cells bit-exact."""
+    c = CONFIGS["C1"]
+    g = _geom(c)
+    x0 = oracle.lattice(c.nx, c.ny, c.nz, g.a)
+    v0 = oracle.velocities(c.n_atoms, c.seed, c.T0)
+    xm, vm, Fm, _ = oracle.run(x0, v0, np.zeros_like(x0), g.b, c.rc, c.dt, 200)
+    e, _ = _engine("C1")
+    e.set_state(xm, vm, Fm)
+    _cells_exact(e, c)
+    e.step(1)
+    x1, v1, F1, e1 = oracle.run(xm, vm, Fm, g.b, c.rc, c.dt, 1)
+    _force_close(e.forces(), F1)
+    assert np.allclose(e.energies()[1][-1, :3], e1[0, :3], rtol=1e-10)
+    e.step(9)
+    x10, v10, F10, e10 = oracle.run(x1, v1, F1, g.b, c.rc, c.dt, 9)
+    assert np.abs(_min_image(e.positions() - x10, g.b)).max() <= 1e-8
+    assert np.abs(e.velocities() - v10).max() <= 1e-8
+    _, en = e.energies()
+    assert np.allclose(en[-9:, 3], e10[:, 3], rtol=1e-10)
+    _cells_exact(e, c)
+
+
+def test_full_size_c4_melted_bench_state():
+    """The exact state bench.py times: C4 from the lattice, melted 200 GPU steps (the
+    bench's --equil default).  Forces of that state (one more step) on 256 sampled
+    atoms against the oracle's all-pairs sums (Q13), every cell and slice bit-exact."""
+    e, c = _engine("C4")
+    g = _geom(c)
+    e.step(200)
+    x = e.positions()
+    _cells_exact(e, c)
+    e.step(1)
+    rng = np.random.default_rng(2)
+    idx = np.sort(rng.choice(c.n_atoms, 256, replace=False))
+    Fo, _ = oracle.forces_subset(x, g.b, c.rc, idx)
+    F = e.forces()[idx]
+    frms = np.sqrt((Fo ** 2).sum(1).mean())
+    err = np.sqrt(((F - Fo) ** 2).sum(1)) / np.maximum(np.sqrt((Fo ** 2).sum(1)), frms)
+    assert err.max() <= 1e-10, err.max()
+    e.close()
+
+
+def test_pair_exactly_at_cutoff():
+    """Inclusive cutoff r^2 <= rc^2 (reading Q5) on the GPU: a pair at exactly
+    rc = 2.5 along x contributes the attractive force 24 (2 rc^-13 - rc^-7) and zero
+    energy, a pair one ulp beyond rc contributes nothing.  Every other atom sits on a
+    simple cubic grid of spacing > rc, more than rc away from the pairs, so the pair
+    terms are the only ones; results against the oracle."""
+    from paper_2507_11289_b200.configs import Config
+    c = Config("cut", 10, 10, 10, 0, rho=0.05)
+    g = _geom(c)
+    n = c.n_atoms
+    pa = np.array([[10.0, 11.0, 12.0], [12.5, 11.0, 12.0],            # exactly rc apart
+                   [30.0, 31.0, 30.0], [np.nextafter(32.5, 40.0), 31.0, 30.0]])   # 1 ulp beyond
+    sp = g.b[0] / 16
+    grid = np.stack(np.meshgrid(*[(np.arange(16) + 0.5) * sp] * 3, indexing="ij"), -1).reshape(-1, 3)
+    far = np.min(np.linalg.norm(grid[:, None, :] - pa[None, :, :], axis=2), axis=1) > 3.0
+    x = np.concatenate([pa, grid[far][: n - 4]])
+    assert x.shape[0] == n and sp > c.rc
+    v = np.zeros_like(x)
+    e, _ = _engine(c)
+    e.set_state(x, v)
+    e.step(1)
+    _, _, Fo, eo = oracle.run(x, v, np.zeros_like(x), g.b, c.rc, c.dt, 1)
+    F = e.forces()
+    mag = 24 * (2 * c.rc ** -13 - c.rc ** -7)
+    assert abs(F[0, 0] - mag) <= 1e-15 and abs(F[1, 0] + mag) <= 1e-15    # atom 0 pulled to +x
+    assert np.all(F[2:] == 0.0) and np.all(Fo[2:] == 0.0)
+    assert np.abs(F - Fo).max() <= 1e-15
+    _, en = e.energies()
+    assert abs(en[0, 0]) <= 1e-15 and abs(en[0, 0] - eo[0, 0]) <= 1e-15
+
+
+def test_first_step_forces_rc4():
+    """rc = 4.0 (C5's long cutoff: ~214 in-cutoff pairs per atom, several hit-list
+    flushes per chunk) on a jittered state: first-step forces within 1e-10 (Q13) and
+    energies within 1e-10 of the oracle."""
+    from paper_2507_11289_b200.configs import Config
+    c = Config("r4", 30, 8, 8, 0, rc=4.0)
+    g = _geom(c)
+    e, _ = _engine(c, seed=3)
+    x = inputs.jitter(oracle.lattice(c.nx, c.ny, c.nz, g.a), g.b, 0.2, 6)
+    v = inputs.gaussian_velocities(c.n_atoms, 0.8, 6)
+    e.set_state(x, v)
+    e.step(1)
+    _, _, Fo, eo = oracle.run(x, v, np.zeros_like(x), g.b, c.rc, c.dt, 1)
+    _force_close(e.forces(), Fo, tol=1e-10)
+    _, en = e.energies()
+    assert np.allclose(en[0, :3], eo[0, :3], rtol=1e-10)

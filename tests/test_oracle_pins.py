@@ -407,3 +407,83 @@ def test_configurational_pressure_is_minus_dU_dVol():
     assert abs(p - p_fd) < 1e-6 * max(1.0, abs(p_fd)), (p, p_fd)
     # ideal-gas limit: no pair within rc -> p = rho T
     assert abs(oracle.pressure(3.0, 0.0, 10, 5.0) - (10 / 5.0) * (2 * 3.0 / 30)) < 1e-15
+
+
+# --------------------------------------------------------------------------- worked examples
+def _three_atom_examples():
+    ex, cur = [], None
+    for row in _golden("three_atom.txt"):
+        if row[0] == "example":
+            cur = {"name": row[1], "F": np.zeros((3, 3))}
+            ex.append(cur)
+        elif row[0] == "pos":
+            cur["pos"] = np.array([float(v) for v in row[1:]]).reshape(3, 3)
+        elif row[0] in ("F0", "F1", "F2"):
+            cur["F"][int(row[0][1])] = [float(v) for v in row[1:]]
+        else:
+            cur[row[0]] = float(row[1])
+    return ex
+
+
+def _exact_three_body(pos, rc):
+    """Exact rational arithmetic of the textbook LJ cluster (Fractions of the fp64
+    inputs): U = sum_{i<j} 4 (s^6 - s^3 + U_shift) with s = 1/r^2, forces from the
+    analytic gradient dU/d(r^2) = 4 (-6 s^7 + 3 s^4), i.e. F_i = -sum_j 2 r_ij dU/d(r^2).
+    Only even powers of r occur, so every value is rational and exact."""
+    from fractions import Fraction as Fr
+    P = [[Fr(v) for v in p] for p in pos]
+    rc2 = Fr(rc) ** 2
+    us = (1 / rc2) ** 3 - (1 / rc2) ** 6
+    F = [[Fr(0)] * 3 for _ in range(3)]
+    U = Fr(0)
+    V = Fr(0)
+    for i in range(3):
+        for j in range(i + 1, 3):
+            d = [P[i][k] - P[j][k] for k in range(3)]
+            r2 = sum(x * x for x in d)
+            if r2 > rc2:
+                continue
+            s = 1 / r2
+            U += 4 * (s ** 6 - s ** 3 + us)
+            V += 2 * s ** 6 - s ** 3
+            dudr2 = 4 * (-6 * s ** 7 + 3 * s ** 4)
+            for k in range(3):
+                F[i][k] -= 2 * d[k] * dudr2
+                F[j][k] += 2 * d[k] * dudr2
+    return np.array([[float(x) for x in f] for f in F]), float(U), float(V)
+
+
+@pytest.mark.parametrize("ex", _three_atom_examples(), ids=lambda e: e["name"])
+def test_three_atom_worked_examples(ex):
+    """SURVEY §8(c) pin 2 (north star: 'two- and three-atom worked examples'):
+    collinear, L-shape and generic triples, golden values to 1e-14 relative.  The
+    golden numbers are first checked against exact rational arithmetic of the
+    textbook potential's gradient (so a typo in the file fails too), then the oracle
+    against the golden numbers.  Catches a dropped pair, a wrong r_ij sign or index,
+    a transposed component, the /2 of P:265/P:267 or a missing U_shift."""
+    Fx, Ux, Vx = _exact_three_body(ex["pos"], RC)
+    scale = max(1.0, np.abs(ex["F"]).max())
+    assert np.abs(Fx - ex["F"]).max() <= 1e-14 * scale
+    assert abs(Ux - ex["U"]) <= 1e-14 * abs(ex["U"])
+    assert abs(Vx - ex["V"]) <= 1e-14 * max(1.0, abs(ex["V"]))
+    F, U, V = oracle.forces(ex["pos"], BIG, RC)
+    assert np.abs(F - ex["F"]).max() <= 1e-14 * scale
+    assert abs(U - ex["U"]) <= 1e-14 * abs(ex["U"])
+    assert abs(V - ex["V"]) <= 1e-14 * max(1.0, abs(ex["V"]))
+
+
+def test_forces_subset_equals_full_rows():
+    """oracle_forces_subset (the sampled reference of the full-size C2/C4 parity) on a
+    shuffled index set with repeats equals the matching rows of the full all-pairs
+    oracle_forces (pinned above), forces and per-atom U bit for bit, on a random box
+    with walls and y/z images.  Catches an idx[k] <-> k mix-up, a wrong output row,
+    a missing minimum image or a dropped self-exclusion."""
+    box = np.array([11.0, 8.1, 7.9])
+    xyz = inputs.random_points(180, box, seed=31, min_sep=0.88)
+    F, U, V, Ui, Vi = oracle.forces(xyz, box, RC, per_atom=True)
+    rng = np.random.default_rng(4)
+    idx = np.concatenate([rng.permutation(180)[:70], [5, 5, 179, 0]])
+    Fs, Us = oracle.forces_subset(xyz, box, RC, idx)
+    assert np.array_equal(Fs, F[idx])
+    assert np.array_equal(Us, Ui[idx])
+    assert Fs.shape == (len(idx), 3)
