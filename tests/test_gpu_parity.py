@@ -431,11 +431,15 @@ def test_pair_exactly_at_cutoff():
     n = c.n_atoms
     pa = np.array([[10.0, 11.0, 12.0], [12.5, 11.0, 12.0],            # exactly rc apart
                    [30.0, 31.0, 30.0], [np.nextafter(32.5, 40.0), 31.0, 30.0]])   # 1 ulp beyond
-    sp = g.b[0] / 16
-    grid = np.stack(np.meshgrid(*[(np.arange(16) + 0.5) * sp] * 3, indexing="ij"), -1).reshape(-1, 3)
+    # one grid plane per slice along x (spacing w), 16 x 16 per plane: every slot holds
+    # at most 256 + 4 atoms
+    ns = g.n_slices
+    gx, gy = g.b[0] / ns, g.b[1] / 16
+    grid = np.stack(np.meshgrid((np.arange(ns) + 0.5) * gx, (np.arange(16) + 0.5) * gy,
+                                (np.arange(16) + 0.5) * gy, indexing="ij"), -1).reshape(-1, 3)
     far = np.min(np.linalg.norm(grid[:, None, :] - pa[None, :, :], axis=2), axis=1) > 3.0
     x = np.concatenate([pa, grid[far][: n - 4]])
-    assert x.shape[0] == n and sp > c.rc
+    assert x.shape[0] == n and min(gx, gy) > c.rc
     v = np.zeros_like(x)
     e, _ = _engine(c)
     e.set_state(x, v)
