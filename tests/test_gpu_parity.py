@@ -441,7 +441,7 @@ def test_pair_exactly_at_cutoff():
     x = np.concatenate([pa, grid[far][: n - 4]])
     assert x.shape[0] == n and min(gx, gy) > c.rc
     v = np.zeros_like(x)
-    e, _ = _engine(c)
+    e, _ = _engine(c, capacity_factor=2.0)   # the start lattice puts two planes in some slices
     e.set_state(x, v)
     e.step(1)
     _, _, Fo, eo = oracle.run(x, v, np.zeros_like(x), g.b, c.rc, c.dt, 1)
