@@ -446,8 +446,8 @@ def test_pair_exactly_at_cutoff():
     e.step(1)
     _, _, Fo, eo = oracle.run(x, v, np.zeros_like(x), g.b, c.rc, c.dt, 1)
     F = e.forces()
-    mag = 24 * (2 * c.rc ** -13 - c.rc ** -7)
-    assert abs(F[0, 0] - mag) <= 1e-15 and abs(F[1, 0] + mag) <= 1e-15    # atom 0 pulled to +x
+    mag = 24 * (2 * c.rc ** -13 - c.rc ** -7)   # F_abs r at rc: negative (attractive)
+    assert abs(F[0, 0] + mag) <= 1e-15 and abs(F[1, 0] - mag) <= 1e-15    # atom 0 pulled to +x
     assert np.all(F[2:] == 0.0) and np.all(Fo[2:] == 0.0)
     assert np.abs(F - Fo).max() <= 1e-15
     _, en = e.energies()
