@@ -313,6 +313,7 @@ def main():
     ap.add_argument("--equil", type=int, default=200, help="untimed melting timesteps before warm-up")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-steady", action="store_true", help="skip the steady-state super-cycle rate (N > 1)")
     ap.add_argument("--hop", default="peer", choices=["peer", "nccl"],
                     help="ring hop: NVLink copy-engine push with stream flags (peer) or NCCL send/recv")
     ap.add_argument("--block", type=int, default=0, help="slices per stage (0 = auto)")
@@ -387,6 +388,31 @@ def main():
     ms = ev0.elapsed_time(ev1)
     st = e.stats()
     D.dsea_set_timing(e.ctx, False)
+
+    # ---- steady state (the paper's metric: molecules processed by all workers in
+    # one super-cycle / super-cycle time): a call of K super-cycles includes the ring's
+    # pipeline fill and drain (rank g starts (2 + W) blocks after rank g-1); a second call
+    # of 2K super-cycles has the same fill and drain, so the difference of the two calls
+    # times K super-cycles alone.  Reported beside the K-cycle value, never instead of it.
+    steady = None
+    if world > 1 and not args.no_steady:
+        barrier()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record()
+        e.step(2 * args.steps * nw)
+        s1.record()
+        barrier()
+        ms2 = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device="cuda")
+        ms1 = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ms1, op=dist.ReduceOp.MAX)
+        dms = float(ms2[0] - ms1[0])
+        if dms > 0:
+            steady = {"value": geo.n_atoms * args.steps * nw / (dms * 1e-3), "unit": "atom-timesteps/s",
+                      "ms_per_super_cycle": dms / args.steps,
+                      "method": f"(T({2 * args.steps} super-cycles) - T({args.steps})) / {args.steps}: "
+                                "one call's pipeline fill and drain cancel (P:344 metric)"}
     t = torch.tensor([ms, float(st.kernel_launches)], dtype=torch.float64, device="cuda")
     if dist is not None:
         tmax = t.clone()
@@ -474,6 +500,7 @@ def main():
                                  "bytes_per_atom": FORCE_BYTES_PER_ATOM},
                          "force_ms_per_launch": force_ms_avg, "force_share_of_step": force_share,
                          "pairs_per_atom": pairs_per_atom},
+            "steady_state": steady,
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "e2e": e2e,

@@ -5,7 +5,7 @@
 // [j0, j0 + nj), each reading its left and right neighbour slices (O_in = 1).
 //
 // A tile is up to TILE_HOME consecutive, z-sorted home atoms of one (cx, cy) column of
-// slice j.  Persistent CTAs (a few per SM) walk the tiles round robin; per tile:
+// slice j.  Persistent CTAs (a few per SM) claim tiles from a counter; per tile:
 //   1. a piece table: 9 neighbour columns x {low z-image, main run, high z-image}, the
 //      cells within one cell (l >= rc) of the home atoms' cells (periodic images in y
 //      and z pre-shifted, x walls: absent columns, readings Q1/Q2).  Warp 0
@@ -97,13 +97,21 @@ __device__ __forceinline__ double lds_f64(unsigned a)
 // come from the column's cell_start (no position loads); the range is halved until its
 // neighbourhood fits the staging capacity.
 __device__ void build_table(const Geo& g, const Tiling& T, const BufView& in, const StgView& stg, int j0,
-                            long long ntiles, int t, int hb, TileTable& A)
+                            long long ntiles, int t, int hb, TileTable& A,
+                            unsigned long long* __restrict__ tile_ctr, unsigned long long ctr_base)
 {
     const int lane = threadIdx.x & 31;
     const int CY = g.cells[1], CZ = g.cells[2];
     int j = 0, tile = 0, cxl = 0, cyi = 0, h1 = 0, colbase_h = 0;
     const int32_t* csj = nullptr;
     for (;;) {
+        if (hb < 0) {   // a new tile: claimed from the launch's counter (CTAs that start late
+                        // -- SMs busy with other kernels -- simply take fewer tiles)
+            unsigned long long c = 0;
+            if (lane == 0) c = atomicAdd(tile_ctr, 1ull) - ctr_base;
+            c = __shfl_sync(FULLMASK, c, 0);
+            t = c >= (unsigned long long)ntiles ? (int)ntiles : (int)c;
+        }
         if (t >= ntiles) {
             if (lane == 0) A.valid = 0;
             return;
@@ -122,7 +130,6 @@ __device__ void build_table(const Geo& g, const Tiling& T, const BufView& in, co
         if (hb < 0) hb = h0;
         if (hb < h1) break;
         if (lane == 0) stg.eatom[(size_t)j * T.tiles + tile] = make_double4(0.0, 0.0, 0.0, 0.0);
-        t += gridDim.x;
         hb = -1;
     }
     // cell (along z) of home atom a: the number of cells c >= 1 of the column with
@@ -215,7 +222,7 @@ __device__ void build_table(const Geo& g, const Tiling& T, const BufView& in, co
 template <bool NVT>
 __global__ void __launch_bounds__(TILE_THREADS, 16 / TILE_WARPS)
 k_force_tile(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt, int j0, int nj,
-             DevErr* __restrict__ err)
+             DevErr* __restrict__ err, unsigned long long* __restrict__ tile_ctr, unsigned long long ctr_base)
 {
     pdl_wait();
     pdl_release();
@@ -223,6 +230,7 @@ k_force_tile(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
     __shared__ TileTable TT[2];
     __shared__ double4 s_ce[TILE_WARPS];        // chunk energy records of the current sub-tile
     __shared__ int s_chunk;                     // next chunk to claim
+    __shared__ int s_tbl;                       // the next table has a builder
     // dynamic shared memory (byte offsets from the host: a base ptxas sees as a constant
     // is rematerialised with S2R/LEA at every hit-list append instead of kept in a register):
     //   off_hl   u16 hit lists [TILE_LM] rows of TILE_ROW bytes (2 per home atom)
@@ -242,7 +250,7 @@ k_force_tile(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
     const size_t zoff = (in.L.off_z - in.L.off_x) / sizeof(double);
     double e_u = 0.0, e_v = 0.0, e_k = 0.0, e_n = 0.0;         // tile record (thread 0)
 
-    if (warp == 0) build_table(g, T, in, stg, j0, ntiles, blockIdx.x, -1, TT[0]);
+    if (warp == 0) build_table(g, T, in, stg, j0, ntiles, 0, -1, TT[0], tile_ctr, ctr_base);
     __syncthreads();
     for (int cur = 0;; cur ^= 1) {
         const TileTable& A = TT[cur];
@@ -306,14 +314,8 @@ k_force_tile(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                 }
             }
         }
-        if (tid == 0) s_chunk = 0;
+        if (tid == 0) { s_chunk = 0; s_tbl = 0; }
         __syncthreads();
-
-        // ---- 1'. the next table (warp 0, overlapping the others' pair work) ------------
-        if (warp == 0) {
-            if (A.he < A.h1) build_table(g, T, in, stg, j0, ntiles, A.t, A.he, TT[cur ^ 1]);
-            else build_table(g, T, in, stg, j0, ntiles, A.t + gridDim.x, -1, TT[cur ^ 1]);
-        }
 
         // ---- 3./4. chunks: screen, pooled FP64 pair work, integration -------------------
         const int nchunks = DSEA_ABL == 1 ? 0 : (nhome + 15) >> 4;
@@ -361,7 +363,8 @@ k_force_tile(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
             // hls + r ROW + 2 a of the shared window (explicit 32-bit shared addresses: one
             // add per access); lane (il, 0) fills rows 0, 1, ... and lane (il, 1) rows
             // M-1, M-2, ... of the same list
-            constexpr int ROW = TILE_ROW, M = TILE_LM;
+            constexpr int ROW = TILE_ROW;
+            const int M = T.maxh;                       // rows in use (<= TILE_LM; tests shrink it)
             const unsigned hls = (unsigned)__cvta_generic_to_shared(hl);
             const int hla = 2 * (warp * 16 + il);
             const int ho0 = hla + (par ? (M - 1) * ROW : 0);
@@ -498,6 +501,15 @@ k_force_tile(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
             // u_core = sum s6 (s6 - 1), vir2 = sum s6 (2 s6 - 1)
             if (lane == 0) s_ce[ch] = make_double4(sa - sb, 2.0 * sa - sb, ke2, pn);
         }
+        // ---- 1'. the next table: built by the first warp out of chunks, overlapping the
+        // others' pair work (which warp builds it does not change its contents)
+        {
+            int own = 0;
+            if (lane == 0) own = atomicExch(&s_tbl, 1) == 0;
+            if (__shfl_sync(FULLMASK, own, 0))
+                build_table(g, T, in, stg, j0, ntiles, A.t, A.he < A.h1 ? A.he : -1, TT[cur ^ 1], tile_ctr,
+                            ctr_base);
+        }
         __syncthreads();
         if (tid == 0) {
             for (int c = 0; c < nchunks; c++) {        // chunk order: independent of the warps
@@ -532,7 +544,7 @@ Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
     Tiling T{};
     T.kind = FORCE_TILE;
     T.home = TILE_HOME;
-    T.maxh = TILE_LM;
+    T.maxh = std::max(8, std::min(TILE_LM, (int)env_num("DSEA_MAXH", TILE_LM)));
     const int CZ = g.cells[2];
     const double mean_col = mean_per_cell * CZ;                // atoms per column
     const double dens = mean_per_cell / g.l[2];                 // atoms per sigma of column
@@ -598,10 +610,15 @@ int force_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t
     // needs the slice's lambda, k_drift)
     const long long ntiles = (long long)nj * T.tiles;
     const unsigned grid = (unsigned)std::min<long long>(ntiles, (long long)T.grid);
+    // the tile counter is never reset: every launch consumes exactly ntiles + grid
+    // increments (each CTA's last claim fails once), so the host tracks each launch's base
     if (g.thermo)
-        launch(k_force_tile<true>, grid, TILE_THREADS, T.smem, s, g, T, in, stg, out_cnt, j0, nj, err);
+        launch(k_force_tile<true>, grid, TILE_THREADS, T.smem, s, g, T, in, stg, out_cnt, j0, nj, err, T.ctr,
+               *T.ctr_base);
     else
-        launch(k_force_tile<false>, grid, TILE_THREADS, T.smem, s, g, T, in, stg, out_cnt, j0, nj, err);
+        launch(k_force_tile<false>, grid, TILE_THREADS, T.smem, s, g, T, in, stg, out_cnt, j0, nj, err, T.ctr,
+               *T.ctr_base);
+    *T.ctr_base += (unsigned long long)ntiles + grid;
     return 1;
 }
 
