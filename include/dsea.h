@@ -242,6 +242,39 @@ dsea_status dsea_set_thermostat(dsea_ctx *ctx, int32_t enable, double T_target);
 dsea_status dsea_get_profiles(dsea_ctx *ctx, dsea_profile *out, int32_t n_slices);
 dsea_status dsea_reset_profiles(dsea_ctx *ctx);
 
+/* ---- thermodynamic observables (NEXT-1; §4.2 validation: u and p) ------ */
+
+/* Per-timestep state point derived from the dsea_energy records (Alg. 1's U, KE, V,
+ * P:250; reading Q24): T = 2 KE / (3 N) (k_B = m = 1, 3N degrees of freedom,
+ * Q9/Q11), u = U / N, e = (U + KE) / N, p = rho T + 24 V / (3 Vol) = rho T + 8 V / Vol
+ * (Alg. 1's V omits the factor 24 of sum r.F; Vol = b_x b_y b_z, rho = N / Vol). */
+typedef struct {
+    int64_t step;
+    double T, p, u, e;
+} dsea_thermo;
+
+/* dsea_energy records in[0..n) of a box of n_atoms atoms and volume `volume` -> out[0..n)
+ * (host only, no context: callers may merge the records of a ring's ranks first).
+ * Caller-owned arrays; in and out may not alias.  DSEA_EINVAL on null pointers with
+ * n > 0, n < 0, n_atoms <= 0 or volume <= 0. */
+dsea_status dsea_thermo_compute(const dsea_energy *in, int64_t n, int64_t n_atoms, double volume,
+                                dsea_thermo *out);
+
+/* x-resolved time averages of one slice ("spatially resolved results";
+ * reading Q24): slice centre x, mean atom count n, number density rho = n / Vol_j,
+ * potential energy per atom u, temperature T = 2 KE / (3 n), pressure
+ * p = rho T + 8 V / Vol_j with Vol_j = w b_y b_z.  Empty slices (n = 0) report u = T = 0. */
+typedef struct {
+    double x, n, rho, u, T, p;
+    int64_t samples;
+} dsea_xprofile;
+
+/* Raw per-slice sums (dsea_get_profiles, summed over a ring's ranks by the caller)
+ * -> averages out[0..n_slices) for the geometry geo (host only).  DSEA_EINVAL on null
+ * pointers or n_slices != geo->n_slices. */
+dsea_status dsea_xprofile_compute(const dsea_profile *raw, int32_t n_slices, const dsea_geometry *geo,
+                                  dsea_xprofile *out);
+
 /* ---- instrumentation ---------------------------------------------------------- */
 
 /* enable != 0: bracket every force launch, bin pass and send with CUDA events on

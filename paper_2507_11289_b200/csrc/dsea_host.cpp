@@ -126,6 +126,10 @@ bool stream_memops_available() { return wait_value32() && write_value32(); }
 namespace {
 struct PeerBlob {
     int32_t magic, rank, ns, pad;
+    // settings every rank must share, or a stream wait is never satisfied and dsea_step
+    // hangs: workers per GPU, block partition (count + hash), plan gap, hop options
+    int32_t W, nblk, plan_gap, flags;
+    uint64_t blocks_hash;
     cudaIpcMemHandle_t in, arr, rel;
 };
 constexpr int32_t PEER_MAGIC = 0x44534541;  // "DSEA"
@@ -1336,6 +1340,22 @@ dsea_status dsea_ring_connect(dsea_ctx* c, const void* ids, int32_t n_ids)
     return DSEA_OK;
 }
 
+// the ring settings a peer blob carries (compared in dsea_ring_connect_peer)
+static void peer_settings(const dsea_ctx* c, PeerBlob& b)
+{
+    b.W = c->W;
+    b.nblk = c->bl.n();
+    b.plan_gap = plan_gap(c->NG, c->W, c->bl);
+    const char* hop = getenv("DSEA_PEER_HOP");
+    const bool ce = !(hop && std::strcmp(hop, "sm") == 0);
+    const char* ctr = getenv("DSEA_RING_COUNTERS");
+    const bool cn = ce && !(ctr && *ctr && atoi(ctr) == 0);
+    b.flags = (ce ? 1 : 0) | (cn ? 2 : 0);
+    uint64_t h = 1469598103934665603ull;                  // FNV-1a of the block starts
+    for (int f : c->bl.first) { h ^= (uint64_t)(uint32_t)f; h *= 1099511628211ull; }
+    b.blocks_hash = h;
+}
+
 dsea_status dsea_ring_export(dsea_ctx* c, void* out, size_t cap, size_t* len)
 {
     if (!c || !len) return DSEA_EINVAL;
@@ -1348,6 +1368,7 @@ dsea_status dsea_ring_export(dsea_ctx* c, void* out, size_t cap, size_t* len)
     b.magic = PEER_MAGIC;
     b.rank = c->rank;
     b.ns = c->g.ns;
+    peer_settings(c, b);
     CUDA_TRY(c, cudaIpcGetMemHandle(&b.in, c->inb.base));
     CUDA_TRY(c, cudaIpcGetMemHandle(&b.arr, c->arr_dev));
     CUDA_TRY(c, cudaIpcGetMemHandle(&b.rel, c->rel_dev));
@@ -1369,6 +1390,17 @@ dsea_status dsea_ring_connect_peer(dsea_ctx* c, const void* blobs, size_t blob_b
     for (int r = 0; r < c->NG; r++)
         if (B[r].magic != PEER_MAGIC || B[r].rank != r || B[r].ns != c->g.ns)
             return fail(c, DSEA_EINVAL, "peer blob %d is not a dsea_ring_export of rank %d", r, r);
+    {
+        PeerBlob mine{};
+        peer_settings(c, mine);
+        for (int r = 0; r < c->NG; r++)
+            if (B[r].W != mine.W || B[r].nblk != mine.nblk || B[r].plan_gap != mine.plan_gap ||
+                B[r].flags != mine.flags || B[r].blocks_hash != mine.blocks_hash)
+                return fail(c, DSEA_EINVAL, "rank %d was sliced or configured differently (W %d/%d, blocks %d/%d, "
+                            "plan gap %d/%d, hop flags %d/%d): every rank needs the same settings",
+                            r, B[r].W, mine.W, B[r].nblk, mine.nblk, B[r].plan_gap, mine.plan_gap, B[r].flags,
+                            mine.flags);
+    }
     void* p = nullptr;
     CUDA_TRY(c, cudaIpcOpenMemHandle(&p, B[succ].in, cudaIpcMemLazyEnablePeerAccess));
     c->succ_in_base = static_cast<char*>(p);
@@ -1430,6 +1462,8 @@ dsea_status dsea_ring_disconnect(dsea_ctx* c)
     return DSEA_OK;
 }
 
+static dsea_status step_chunk(dsea_ctx* c, int64_t n_steps);
+
 dsea_status dsea_step(dsea_ctx* c, int64_t n_steps)
 {
     if (!c) return DSEA_EINVAL;
@@ -1438,6 +1472,23 @@ dsea_status dsea_step(dsea_ctx* c, int64_t n_steps)
     if (c->NG > 1 && !c->connected) return fail(c, DSEA_ESTATE, "ring not connected (dsea_ring_connect)");
     if (n_steps == 0) return DSEA_OK;
     CUDA_TRY(c, cudaSetDevice(c->device));
+    // bounded memory for any n: the call runs in chunks of whole super-cycles (at most
+    // ~64 MB of per-(slice, timestep) energy records and a bounded stage plan each); the
+    // ring's counters carry across chunks exactly as across calls, so the result equals
+    // one call (and a chunk boundary costs one pipeline fill of the ring)
+    const int64_t nw = (int64_t)c->NG * c->W;
+    const int64_t max_steps = std::max<int64_t>(nw, ((64ll << 20) / ((int64_t)sizeof(UnitEnergy) * c->g.ns)) / nw * nw);
+    for (int64_t done = 0; done < n_steps;) {
+        const int64_t n = std::min(max_steps, n_steps - done);
+        dsea_status s = step_chunk(c, n);
+        if (s) return s;
+        done += n;
+    }
+    return DSEA_OK;
+}
+
+static dsea_status step_chunk(dsea_ctx* c, int64_t n_steps)
+{
     const int ns = c->g.ns;
     const int64_t nw = (int64_t)c->NG * c->W;
     const int64_t rows = ((n_steps + nw - 1) / nw) * nw;
@@ -1593,6 +1644,43 @@ dsea_status dsea_reset_profiles(dsea_ctx* c)
 {
     if (!c) return DSEA_EINVAL;
     for (auto& p : c->prof) p = dsea_profile{};
+    return DSEA_OK;
+}
+
+dsea_status dsea_thermo_compute(const dsea_energy* in, int64_t n, int64_t n_atoms, double volume, dsea_thermo* out)
+{
+    if (n < 0 || n_atoms <= 0 || !(volume > 0.0) || (n > 0 && (!in || !out))) return DSEA_EINVAL;
+    const double N = (double)n_atoms, rho = N / volume;
+    for (int64_t i = 0; i < n; i++) {
+        const dsea_energy& e = in[i];
+        dsea_thermo& t = out[i];
+        t.step = e.step;
+        t.T = 2.0 * e.KE / (3.0 * N);                      // k_B = m = 1, 3N dof (Q9, Q11)
+        t.p = rho * t.T + 24.0 * e.V / (3.0 * volume);     // Alg. 1's V: sum r.F = 24 V (Q24)
+        t.u = e.U / N;
+        t.e = (e.U + e.KE) / N;
+    }
+    return DSEA_OK;
+}
+
+dsea_status dsea_xprofile_compute(const dsea_profile* raw, int32_t n_slices, const dsea_geometry* geo,
+                                  dsea_xprofile* out)
+{
+    if (!raw || !geo || !out || n_slices != geo->n_slices || n_slices < 1) return DSEA_EINVAL;
+    const double vol = geo->w * geo->b[1] * geo->b[2];    // slice volume
+    for (int j = 0; j < n_slices; j++) {
+        const dsea_profile& r = raw[j];
+        dsea_xprofile& o = out[j];
+        const double s = r.samples > 0 ? (double)r.samples : 1.0;
+        const double n = r.n_sum / s, ke = r.KE_sum / s, U = r.U_sum / s, V = r.V_sum / s;
+        o.x = (j + 0.5) * geo->w;
+        o.n = n;
+        o.rho = n / vol;
+        o.T = n > 0 ? 2.0 * ke / (3.0 * n) : 0.0;
+        o.u = n > 0 ? U / n : 0.0;
+        o.p = o.rho * o.T + 24.0 * V / (3.0 * vol);
+        o.samples = r.samples;
+    }
     return DSEA_OK;
 }
 

@@ -67,6 +67,17 @@ class dsea_profile(ctypes.Structure):
                 ("V_sum", ctypes.c_double), ("KE_sum", ctypes.c_double)]
 
 
+class dsea_thermo(ctypes.Structure):
+    _fields_ = [("step", ctypes.c_int64), ("T", ctypes.c_double), ("p", ctypes.c_double),
+                ("u", ctypes.c_double), ("e", ctypes.c_double)]
+
+
+class dsea_xprofile(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_double), ("n", ctypes.c_double), ("rho", ctypes.c_double),
+                ("u", ctypes.c_double), ("T", ctypes.c_double), ("p", ctypes.c_double),
+                ("samples", ctypes.c_int64)]
+
+
 class dsea_stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_int64), ("force_launches", ctypes.c_int64),
                 ("atom_steps", ctypes.c_int64), ("force_ms", ctypes.c_double),
@@ -102,6 +113,10 @@ SIGNATURES = [
     ("dsea_set_thermostat", _st, [_c, ctypes.c_int32, ctypes.c_double]),
     ("dsea_get_profiles", _st, [_c, ctypes.POINTER(dsea_profile), ctypes.c_int32]),
     ("dsea_reset_profiles", _st, [_c]),
+    ("dsea_thermo_compute", _st, [ctypes.POINTER(dsea_energy), ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                  ctypes.POINTER(dsea_thermo)]),
+    ("dsea_xprofile_compute", _st, [ctypes.POINTER(dsea_profile), ctypes.c_int32, ctypes.POINTER(dsea_geometry),
+                                    ctypes.POINTER(dsea_xprofile)]),
     ("dsea_set_timing", _st, [_c, ctypes.c_int32]),
     ("dsea_get_stats", _st, [_c, ctypes.POINTER(dsea_stats)]),
     ("dsea_reset_stats", _st, [_c]),
@@ -269,6 +284,46 @@ def dsea_get_cells(ctx, n_atoms):
 _ENERGY_DT = np.dtype([("step", np.int64), ("U", np.float64), ("KE", np.float64), ("V", np.float64)])
 
 
+def dsea_get_energy_records(ctx):
+    """The raw dsea_energy records (structured array: step, U, KE, V) of this rank."""
+    n = ctypes.c_int64()
+    cap = 4096
+    while True:
+        rec = np.zeros(cap, dtype=_ENERGY_DT)
+        _check(ctx, lib.dsea_get_energies(ctx, rec.ctypes.data_as(ctypes.POINTER(dsea_energy)), cap,
+                                          ctypes.byref(n)))
+        if n.value < cap:
+            return rec[:n.value]
+        cap *= 4
+
+
+_THERMO_DT = np.dtype([("step", np.int64), ("T", np.float64), ("p", np.float64), ("u", np.float64),
+                       ("e", np.float64)])
+_XPROF_DT = np.dtype([("x", np.float64), ("n", np.float64), ("rho", np.float64), ("u", np.float64),
+                      ("T", np.float64), ("p", np.float64), ("samples", np.int64)])
+
+
+def dsea_thermo_compute(records, n_atoms, volume):
+    """Per-timestep T, p, u, e of dsea_energy records (the library's dsea_thermo_compute);
+    returns a dict of arrays."""
+    rec = np.ascontiguousarray(records, dtype=_ENERGY_DT)
+    out = np.zeros(rec.shape[0], dtype=_THERMO_DT)
+    _check(None, lib.dsea_thermo_compute(rec.ctypes.data_as(ctypes.POINTER(dsea_energy)), rec.shape[0],
+                                         int(n_atoms), float(volume),
+                                         out.ctypes.data_as(ctypes.POINTER(dsea_thermo))))
+    return {k: out[k].copy() for k in _THERMO_DT.names}
+
+
+def dsea_xprofile_compute(raw, geo):
+    """Per-slice time averages (the library's dsea_xprofile_compute) of raw per-slice
+    sums for geometry geo (a dsea_geometry); returns a dict of arrays."""
+    rec = np.ascontiguousarray(raw, dtype=_PROFILE_DT)
+    out = np.zeros(rec.shape[0], dtype=_XPROF_DT)
+    _check(None, lib.dsea_xprofile_compute(rec.ctypes.data_as(ctypes.POINTER(dsea_profile)), rec.shape[0],
+                                           ctypes.byref(geo), out.ctypes.data_as(ctypes.POINTER(dsea_xprofile))))
+    return {k: out[k].copy() for k in _XPROF_DT.names}
+
+
 def dsea_get_energies(ctx):
     """(steps[n], [n, 4] = {U, KE, V, E = U + KE}) of every timestep this rank computed."""
     n = ctypes.c_int64()
@@ -393,38 +448,36 @@ class Engine:
     def energies(self):
         return dsea_get_energies(self.ctx)
 
+    def _energy_records(self):
+        return dsea_get_energy_records(self.ctx)
+
+    def _geometry_struct(self):
+        return dsea_get_geometry(self.ctx)
+
     def set_state(self, xyz, v, f=None):
         dsea_set_state(self.ctx, xyz, v, f)
 
     def set_thermostat(self, T_target):
         dsea_set_thermostat(self.ctx, T_target)
 
-    def pressure(self):
-        """Per-timestep virial pressure p = rho T + 24 V / (3 Vol), T = 2 KE / (3 N)
-        (Alg. 1's V; reading Q24)."""
+    def thermo(self):
+        """Per-timestep T, p, u, e (dsea_thermo_compute: p = rho T + 24 V / (3 Vol), Alg. 1's
+        V; reading Q24) as a dict of arrays keyed by name."""
         g = self.geometry
-        vol = g.b[0] * g.b[1] * g.b[2]
-        _, e = self.energies()
-        n = self.n_atoms
-        return (n / vol) * (2.0 * e[:, 1] / (3.0 * n)) + 24.0 * e[:, 2] / (3.0 * vol)
+        return dsea_thermo_compute(self._energy_records(), self.n_atoms, g.b[0] * g.b[1] * g.b[2])
+
+    def pressure(self):
+        """Per-timestep virial pressure p = rho T + 24 V / (3 Vol), T = 2 KE / (3 N)."""
+        return self.thermo()["p"]
 
     def raw_profiles(self):
         return dsea_get_profiles(self.ctx, self.geometry.n_slices)
 
     def profiles(self, raw=None):
-        """x-resolved time averages per slice (Q24): slice centre x, atom
-        count n, density rho, potential energy per atom u, temperature T, pressure p."""
-        g = self.geometry
-        r = self.raw_profiles() if raw is None else raw
-        vol = g.w * g.b[1] * g.b[2]
-        s = np.maximum(r["samples"], 1)
-        n = r["n_sum"] / s
-        ke, U, V = r["KE_sum"] / s, r["U_sum"] / s, r["V_sum"] / s
-        with np.errstate(invalid="ignore", divide="ignore"):
-            T = np.where(n > 0, 2.0 * ke / (3.0 * n), 0.0)
-            u = np.where(n > 0, U / n, 0.0)
-        return {"x": (np.arange(g.n_slices) + 0.5) * g.w, "n": n, "rho": n / vol, "u": u, "T": T,
-                "p": (n / vol) * T + 24.0 * V / (3.0 * vol), "samples": r["samples"]}
+        """x-resolved time averages per slice (Q24) from dsea_xprofile_compute:
+        slice centre x, atom count n, density rho, potential energy per atom u,
+        temperature T, pressure p.  raw: per-slice sums (e.g. summed over ring ranks)."""
+        return dsea_xprofile_compute(self.raw_profiles() if raw is None else raw, self._geometry_struct())
 
     def reset_profiles(self):
         dsea_reset_profiles(self.ctx)

@@ -1,0 +1,143 @@
+"""NEXT-1: validation-grade thermodynamics at the paper's validation
+state point (§4.2: NVT, T* = 1.5, rho* = 0.5, truncated-and-shifted LJ with
+rc = 2.5; the paper compares DSEAmd at N = 1e8 with ms2 at N = 2048: u within ~0.1 %,
+p within ~0.01 %, p rising ~0.03 % near the mirror walls).
+
+Here: the GPU engine at large N against the CPU oracle at N = 2048 (the ms2 size) --
+both with the x mirror walls of the method, both through their per-slice records, the
+bulk taken as the slices more than `--skin` sigma from either wall.  Statistical errors
+from block averages.  Also the GPU's x-resolved pressure, density, u and T profiles
+(dsea_xprofile_compute) for the near-wall behaviour.
+
+  python scripts/validate_thermo.py [--out profiles/r02/thermo_validation.json]
+Needs a B200 (GPU part) and the host cores (oracle part)."""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+from paper_2507_11289_b200 import dsea as D  # noqa: E402
+
+T_STAR, RHO, RC, DT = 1.5, 0.5, 2.5, 0.0018
+
+
+def bulk_state(n, U, V, KE, vol):
+    """u, p, T of summed slice records {n, U, V, KE} over a region of volume vol."""
+    T = 2.0 * KE / (3.0 * n)
+    return U / n, (n / vol) * T + 24.0 * V / (3.0 * vol), T
+
+
+def mean_sem(x):
+    x = np.asarray(x, dtype=np.float64)
+    return float(x.mean()), float(x.std(ddof=1) / np.sqrt(len(x))) if len(x) > 1 else 0.0
+
+
+def gpu_part(nx, ny, nz, equil, blocks, block_steps, skin):
+    e = D.Engine(D.Box(nx, ny, nz, RHO, RC, DT, T_STAR, 20250507))
+    e.slice(n_slices=0)
+    g = e.geometry
+    e.set_thermostat(T_STAR)
+    t0 = time.time()
+    e.step(equil)
+    ns = g.n_slices
+    xc = (np.arange(ns) + 0.5) * g.w
+    bulk = (xc > skin) & (xc < g.b[0] - skin)
+    vol_b = bulk.sum() * g.w * g.b[1] * g.b[2]
+    res, prof_sum = [], None
+    for _ in range(blocks):
+        e.reset_profiles()
+        e.step(block_steps)
+        r = e.raw_profiles()
+        s = r["samples"][bulk][0]
+        res.append(bulk_state(r["n_sum"][bulk].sum() / s, r["U_sum"][bulk].sum() / s,
+                              r["V_sum"][bulk].sum() / s, r["KE_sum"][bulk].sum() / s, vol_b))
+        if prof_sum is None:
+            prof_sum = r.copy()
+        else:
+            for k in ("samples", "n_sum", "U_sum", "V_sum", "KE_sum"):
+                prof_sum[k] += r[k]
+    th = e.thermo()
+    nsamp = blocks * block_steps
+    whole = {"u": mean_sem(th["u"][-nsamp:]), "p": mean_sem(th["p"][-nsamp:]), "T": mean_sem(th["T"][-nsamp:])}
+    xp = e.profiles(prof_sum)
+    out = {"n_atoms": int(g.n_atoms), "box": list(g.b), "n_slices": int(ns), "slice_width": g.w,
+           "equil_steps": equil, "sample_steps": nsamp, "blocks": blocks, "bulk_slices": int(bulk.sum()),
+           "bulk_skin_sigma": skin, "seconds": time.time() - t0,
+           "bulk": {k: mean_sem([r[i] for r in res]) for i, k in enumerate(("u", "p", "T"))},
+           "whole_box_per_step": whole,
+           "profile": {k: [float(v) for v in xp[k]] for k in ("x", "rho", "u", "T", "p")}}
+    e.close()
+    return out
+
+
+def oracle_part(nx, ny, nz, equil, blocks, block_steps, skin):
+    g = oracle.geometry(nx, ny, nz, RHO, RC, 0, 1)
+    x = oracle.lattice(nx, ny, nz, g.a)
+    v = oracle.velocities(x.shape[0], 20250507, T_STAR)
+    F = np.zeros_like(x)
+    t0 = time.time()
+    x, v, F, _, _ = oracle.run_ex(x, v, F, g.b, RC, DT, equil, g, T_target=T_STAR)
+    ns = int(g.n_slices)
+    w = g.b[0] / ns
+    xc = (np.arange(ns) + 0.5) * w
+    bulk = (xc > skin) & (xc < g.b[0] - skin)
+    vol_b = bulk.sum() * w * g.b[1] * g.b[2]
+    res = []
+    for _ in range(blocks):
+        x, v, F, _, rec = oracle.run_ex(x, v, F, g.b, RC, DT, block_steps, g, T_target=T_STAR)
+        m = rec[:, bulk, :].sum(axis=1).mean(axis=0)       # time average of the bulk sums {n, U, V, KE}
+        res.append(bulk_state(m[0], m[1], m[2], m[3], vol_b))
+    return {"n_atoms": int(x.shape[0]), "box": list(g.b), "n_slices": ns, "equil_steps": equil,
+            "sample_steps": blocks * block_steps, "blocks": blocks, "bulk_slices": int(bulk.sum()),
+            "bulk_skin_sigma": skin, "threads": oracle.num_threads(), "seconds": time.time() - t0,
+            "bulk": {k: mean_sem([r[i] for r in res]) for i, k in enumerate(("u", "p", "T"))}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "thermo_validation.json"))
+    ap.add_argument("--gpu-cells", default="120,24,24", help="FCC cells of the GPU box (rho 0.5: a = 2)")
+    ap.add_argument("--oracle-cells", default="16,8,4", help="FCC cells of the oracle box (N = 2048)")
+    ap.add_argument("--equil", type=int, default=3000)
+    ap.add_argument("--blocks", type=int, default=10)
+    ap.add_argument("--gpu-block-steps", type=int, default=1500)
+    ap.add_argument("--oracle-block-steps", type=int, default=2000)
+    ap.add_argument("--skin", type=float, default=8.0, help="bulk = slices this far from both walls")
+    a = ap.parse_args()
+    gc = [int(v) for v in a.gpu_cells.split(",")]
+    oc = [int(v) for v in a.oracle_cells.split(",")]
+    gpu = gpu_part(*gc, a.equil, a.blocks, a.gpu_block_steps, a.skin)
+    orc = oracle_part(*oc, a.equil, a.blocks, a.oracle_block_steps, a.skin)
+    cmp = {}
+    for k in ("u", "p", "T"):
+        (mg, sg), (mo, so) = gpu["bulk"][k], orc["bulk"][k]
+        d = mg - mo
+        cmp[k] = {"gpu": mg, "oracle": mo, "rel_diff": d / abs(mo), "combined_sem": float(np.hypot(sg, so)),
+                  "z": float(d / np.hypot(sg, so)) if np.hypot(sg, so) > 0 else None}
+    # near-wall pressure: the outermost slices against the bulk mean of the GPU profile
+    p = np.array(gpu["profile"]["p"])
+    xc = np.array(gpu["profile"]["x"])
+    bulk = (xc > a.skin) & (xc < gpu["box"][0] - a.skin)
+    pb = p[bulk].mean()
+    wall = {"p_bulk": float(pb), "p_first_slice_rel": float(p[0] / pb - 1.0),
+            "p_last_slice_rel": float(p[-1] / pb - 1.0),
+            "p_within_skin_rel": float(p[~bulk].mean() / pb - 1.0)}
+    out = {"state": {"T": T_STAR, "rho": RHO, "rc": RC, "dt": DT, "ensemble": "NVT (per-slice isokinetic, Q23)",
+                     "potential": "LJ 12-6 truncated and shifted at rc (Q6)"},
+           "gpu": gpu, "oracle": orc, "comparison_bulk": cmp, "near_wall": wall,
+           "paper": "P:328-332: u within ~0.1 %, p within ~0.01 % of ms2 (N = 2048); p ~0.03 % higher near the walls"}
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps({"comparison_bulk": cmp, "near_wall": wall}, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -192,3 +192,46 @@ def test_eq1_nmax_reported():
     for ns, W in [(100, 1), (64, 2), (109, 1), (256, 15)]:
         st, g = D.dsea_geometry_compute(4 * ns // 3 + 10, 5, 5, 0.8, 2.5, n_slices=ns, workers_per_gpu=W)
         assert g.n_max == oracle.nmax(ns, W)
+
+
+def test_thermo_compute_matches_oracle_pressure():
+    """dsea_thermo_compute (host-only ABI call; NEXT-1 observables, Q24) against the
+    oracle's independent pressure definition and the plain T, u, e formulas."""
+    rng = np.random.default_rng(3)
+    rec = np.zeros(7, dtype=D._ENERGY_DT)
+    rec["step"] = np.arange(7) + 40
+    rec["U"] = -5.0 * 1000 + rng.random(7)
+    rec["KE"] = 1500.0 + rng.random(7)
+    rec["V"] = -900.0 + rng.random(7)
+    n, vol = 1000, 1250.0
+    t = D.dsea_thermo_compute(rec, n, vol)
+    assert np.array_equal(t["step"], rec["step"])
+    assert np.allclose(t["p"], oracle.pressure(rec["KE"], rec["V"], n, vol), rtol=1e-14)
+    assert np.allclose(t["T"], 2 * rec["KE"] / (3 * n), rtol=1e-15)
+    assert np.allclose(t["u"], rec["U"] / n, rtol=1e-15)
+    assert np.allclose(t["e"], (rec["U"] + rec["KE"]) / n, rtol=1e-15)
+    with pytest.raises(D.DseaError):
+        D.dsea_thermo_compute(rec, 0, vol)
+
+
+def test_xprofile_compute_matches_oracle_pressure():
+    """dsea_xprofile_compute: per-slice averages and pressure (slice volume w b_y b_z)
+    against the oracle's pressure of the averaged sums; empty slices report zeros."""
+    st, g = D.dsea_geometry_compute(20, 10, 5, 0.8, 2.5, n_slices=8)
+    assert st == 0
+    raw = np.zeros(8, dtype=D._PROFILE_DT)
+    raw["samples"] = 10
+    raw["n_sum"] = 500.0 * 10
+    raw["n_sum"][3] = 0.0
+    raw["U_sum"] = -2900.0 * 10
+    raw["V_sum"] = -480.0 * 10
+    raw["KE_sum"] = 360.0 * 10
+    raw["U_sum"][3] = raw["V_sum"][3] = raw["KE_sum"][3] = 0.0
+    x = D.dsea_xprofile_compute(raw, g)
+    vol = g.w * g.b[1] * g.b[2]
+    ok = np.arange(8) != 3
+    assert np.allclose(x["p"], oracle.pressure(raw["KE_sum"] / 10, raw["V_sum"] / 10, raw["n_sum"] / 10, vol),
+                       rtol=1e-14)
+    assert np.allclose(x["x"], (np.arange(8) + 0.5) * g.w)
+    assert np.allclose(x["u"][ok], -2900.0 / 500.0) and x["u"][3] == 0.0 and x["T"][3] == 0.0
+    assert np.allclose(x["rho"], raw["n_sum"] / 10 / vol)
