@@ -3,11 +3,15 @@ state point (§4.2: NVT, T* = 1.5, rho* = 0.5, truncated-and-shifted L
 rc = 2.5; the paper compares DSEAmd at N = 1e8 with ms2 at N = 2048: u within ~0.1 %,
 p within ~0.01 %, p rising ~0.03 % near the mirror walls).
 
-Here: the GPU engine at large N against the CPU oracle at N = 2048 (the ms2 size) --
-both with the x mirror walls of the method, both through their per-slice records, the
-bulk taken as the slices more than `--skin` sigma from either wall.  Statistical errors
-from block averages.  Also the GPU's x-resolved pressure, density, u and T profiles
-(dsea_xprofile_compute) for the near-wall behaviour.
+Here, all with the x mirror walls of the method and through per-slice records, the
+bulk taken as the slices more than `--skin` sigma from either wall, statistical errors
+from block averages:
+  * GPU and CPU oracle on the SAME N = 2048 box (the ms2 size): the same model, so
+    their bulk u, p, T must agree within the statistical error (a thermodynamic-level
+    check of the engine beyond trajectory parity);
+  * the GPU at large N: the finite-size shift of the N = 2048 values, and the
+    x-resolved pressure, density, u and T profiles (dsea_xprofile_compute) near the
+    walls.
 
   python scripts/validate_thermo.py [--out profiles/r02/thermo_validation.json]
 Needs a B200 (GPU part) and the host cores (oracle part)."""
@@ -104,23 +108,31 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "thermo_validation.json"))
     ap.add_argument("--gpu-cells", default="120,24,24", help="FCC cells of the GPU box (rho 0.5: a = 2)")
-    ap.add_argument("--oracle-cells", default="16,8,4", help="FCC cells of the oracle box (N = 2048)")
+    ap.add_argument("--oracle-cells", default="8,8,8", help="FCC cells of the small box (N = 2048)")
     ap.add_argument("--equil", type=int, default=3000)
     ap.add_argument("--blocks", type=int, default=10)
     ap.add_argument("--gpu-block-steps", type=int, default=1500)
     ap.add_argument("--oracle-block-steps", type=int, default=2000)
-    ap.add_argument("--skin", type=float, default=8.0, help="bulk = slices this far from both walls")
+    ap.add_argument("--skin", type=float, default=8.0, help="bulk = slices this far from both walls (large box)")
+    ap.add_argument("--small-skin", type=float, default=4.0, help="the same for the N = 2048 box")
+    ap.add_argument("--small-gpu-block-steps", type=int, default=20000)
     a = ap.parse_args()
     gc = [int(v) for v in a.gpu_cells.split(",")]
     oc = [int(v) for v in a.oracle_cells.split(",")]
     gpu = gpu_part(*gc, a.equil, a.blocks, a.gpu_block_steps, a.skin)
-    orc = oracle_part(*oc, a.equil, a.blocks, a.oracle_block_steps, a.skin)
-    cmp = {}
-    for k in ("u", "p", "T"):
-        (mg, sg), (mo, so) = gpu["bulk"][k], orc["bulk"][k]
-        d = mg - mo
-        cmp[k] = {"gpu": mg, "oracle": mo, "rel_diff": d / abs(mo), "combined_sem": float(np.hypot(sg, so)),
-                  "z": float(d / np.hypot(sg, so)) if np.hypot(sg, so) > 0 else None}
+    gpu_small = gpu_part(*oc, a.equil, a.blocks, a.small_gpu_block_steps, a.small_skin)
+    orc = oracle_part(*oc, a.equil, a.blocks, a.oracle_block_steps, a.small_skin)
+
+    def compare(A, B, na, nb):
+        out = {}
+        for k in ("u", "p", "T"):
+            (ma, sa), (mb, sb) = A["bulk"][k], B["bulk"][k]
+            d = ma - mb
+            out[k] = {na: ma, nb: mb, "rel_diff": d / abs(mb), "combined_sem": float(np.hypot(sa, sb)),
+                      "z": float(d / np.hypot(sa, sb)) if np.hypot(sa, sb) > 0 else None}
+        return out
+    cmp = {"gpu_vs_oracle_same_box_N2048": compare(gpu_small, orc, "gpu", "oracle"),
+           "gpu_large_vs_oracle_N2048": compare(gpu, orc, "gpu_large", "oracle")}
     # near-wall pressure: the outermost slices against the bulk mean of the GPU profile
     p = np.array(gpu["profile"]["p"])
     xc = np.array(gpu["profile"]["x"])
@@ -131,7 +143,7 @@ def main():
             "p_within_skin_rel": float(p[~bulk].mean() / pb - 1.0)}
     out = {"state": {"T": T_STAR, "rho": RHO, "rc": RC, "dt": DT, "ensemble": "NVT (per-slice isokinetic, Q23)",
                      "potential": "LJ 12-6 truncated and shifted at rc (Q6)"},
-           "gpu": gpu, "oracle": orc, "comparison_bulk": cmp, "near_wall": wall,
+           "gpu_large": gpu, "gpu_small": gpu_small, "oracle": orc, "comparison_bulk": cmp, "near_wall": wall,
            "paper": "P:328-332: u within ~0.1 %, p within ~0.01 % of ms2 (N = 2048); p ~0.03 % higher near the walls"}
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as f:
