@@ -314,6 +314,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-steady", action="store_true", help="skip the steady-state super-cycle rate (N > 1)")
+    ap.add_argument("--staged", action="store_true",
+                    help="force the staged schedule on one GPU (the ring of one: the baseline of ring efficiency)")
     ap.add_argument("--hop", default="peer", choices=["peer", "nccl"],
                     help="ring hop: NVLink copy-engine push with stream flags (peer) or NCCL send/recv")
     ap.add_argument("--block", type=int, default=0, help="slices per stage (0 = auto)")
@@ -352,7 +354,8 @@ def main():
     W = args.workers
     e = D.Engine(D.Box(cfg.nx, cfg.ny, cfg.nz, cfg.rho, cfg.rc, cfg.dt, cfg.T0, cfg.seed))
     e.slice(n_slices=cfg.n_slices, cells_per_slice_x=cfg.cells_per_slice_x, n_gpus=world, rank=rank,
-            device=local_rank, workers_per_gpu=W, slices_per_stage=args.block)
+            device=local_rank, workers_per_gpu=W, slices_per_stage=args.block,
+            mode=D.DSEA_MODE_STAGED if args.staged else D.DSEA_MODE_AUTO)
     if args.thermostat > 0:
         e.set_thermostat(args.thermostat)
     if world > 1:
@@ -484,7 +487,7 @@ def main():
                        "cells": list(geo.cells), "rho": cfg.rho, "rc": cfg.rc, "dt": cfg.dt,
                        "workers_per_gpu": W, "timesteps_per_step": nw,
                        "ensemble": f"NVT(T={args.thermostat})" if args.thermostat > 0 else "NVE",
-                       "mode": "fused" if world == 1 and W == 1 else "staged-ring",
+                       "mode": "fused" if world == 1 and W == 1 and not args.staged else "staged-ring",
                        "l2": "inputs larger than L2 (state %.2f GB)" % (atoms * 76 / 1e9),
                        "parallelism": f"ring{world}", "ring_hop": args.hop if world > 1 else None},
             "roofline": {"bound": "alu", "achieved": fp64_achieved, "peak": fp64_peak,
