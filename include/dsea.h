@@ -216,6 +216,17 @@ dsea_status dsea_get_forces(dsea_ctx *ctx, double *fxyz, int64_t n_atoms);
  * cell_xyz[3*n] = global cell (x, y, z), slice[n] = slice index. */
 dsea_status dsea_get_cells(dsea_ctx *ctx, int32_t *cell_xyz, int32_t *slice, int64_t n_atoms);
 
+/* The contents of one slice (the paper's "store slices", §3.1, one slot at a
+ * time -- for states too large to gather by id, NEXT-3): the atoms of slice j in slot
+ * order (cell-sorted, Q21): positions xyz[3n], velocities vxyz[3n], F_new of the last
+ * force pass fxyz[3n] (any of the three may be NULL) and ids[n] (may be NULL).  Writes
+ * min(cap, n_j) atoms; *n_written = n_j (call with cap = 0 to size the arrays).
+ * Caller-owned arrays.  DSEA_EINVAL for j outside [0, N_S) or a null n_written;
+ * DSEA_ESTATE before dsea_slice or on a rank that does not hold the state (rank 0 of a
+ * ring holds it between calls, Q22). */
+dsea_status dsea_get_slice(dsea_ctx *ctx, int32_t j, double *xyz, double *vxyz, double *fxyz, int32_t *ids,
+                           int64_t cap, int64_t *n_written);
+
 /* Energies of every timestep this rank computed since dsea_init, in step order.
  * Writes min(cap, available) records; *n_written gets the count written. */
 dsea_status dsea_get_energies(dsea_ctx *ctx, dsea_energy *out, int64_t cap, int64_t *n_written);

@@ -477,7 +477,7 @@ k_force_tile(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                 const double vy = vy0 + (Fy + fyo) * hdt;
                 const double vz = vz0 + (Fz + fzo) * hdt;
                 ke2 = vx * vx + vy * vy + vz * vz;
-                const size_t st = (size_t)j * g.cap + gi;
+                const size_t st = stg_index(stg, j, g.cap, gi);
                 if (NVT) {
                     // NVT: the slice's scale factor needs every atom's kick first
                     // (k_energy -> lambda_j, then k_drift finishes md_v3b)

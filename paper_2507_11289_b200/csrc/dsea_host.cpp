@@ -332,15 +332,19 @@ struct dsea_ctx {
     size_t e_cap = 0;
     DevErr* err_dev = nullptr;
     unsigned long long* tile_ctr = nullptr;
-    double* aos_dev = nullptr;            // [3 * 3N] by-id AoS scratch for set_state / get_*
+    double* aos_dev = nullptr;            // by-id AoS scratch for set_state (per slice group) / get_* (3N)
+    size_t aos_cap = 0;                   // doubles in aos_dev
+    int32_t* ids_dev = nullptr;           // atom ids of an upload group
+    int stg_pool = 0;                     // slices per staging buffer (StgView.pool)
+    int out_pool = 0;                     // slots of the last worker's local output buffer
+    std::vector<cudaEvent_t> ev_pslot;    // per slot of that pool: its last hop (push / send) done
+    std::vector<char> pslot_rec;
     unsigned long long* count_dev = nullptr;
     unsigned long long tile_ctr_base = 0;
     std::vector<cudaEvent_t> ev_recv, ev_free, ev_bin, ev_send;
     std::vector<cudaEvent_t> ev_force;              // per worker: force done
     std::vector<cudaEvent_t> ev_energy;             // per (worker, block): energies of the block reduced
     std::vector<cudaEvent_t> ev_binblk;             // per block: last remote bin run done
-    std::vector<cudaEvent_t> ev_hop;                // per block: copy-engine hop of the last run done
-    std::vector<char> hop_rec;                      // ev_hop[k] has been recorded
     bool ce_hop = false;                            // peer hop: local bin + copy engine (default)
     cudaEvent_t ev_cs = nullptr;                    // compute-stream point for the bin stream
 
@@ -545,6 +549,9 @@ void free_device(dsea_ctx* c)
     }
     for (void* p : c->dallocs) cudaFree(p);
     c->dallocs.clear();
+    c->aos_dev = nullptr; c->aos_cap = 0; c->ids_dev = nullptr; c->count_dev = nullptr;
+    for (cudaEvent_t e : c->ev_pslot) cudaEventDestroy(e);
+    c->ev_pslot.clear(); c->pslot_rec.clear();
     for (auto* v : {&c->ev_recv, &c->ev_free, &c->ev_bin, &c->ev_send})
         for (cudaEvent_t e : *v) cudaEventDestroy(e);
     c->ev_recv.clear(); c->ev_free.clear(); c->ev_bin.clear(); c->ev_send.clear();
@@ -559,9 +566,6 @@ void free_device(dsea_ctx* c)
     if (c->bs) cudaStreamDestroy(c->bs);
     for (cudaEvent_t e : c->ev_binblk) cudaEventDestroy(e);
     c->ev_binblk.clear();
-    for (cudaEvent_t e : c->ev_hop) cudaEventDestroy(e);
-    c->ev_hop.clear();
-    c->hop_rec.clear();
     if (c->ev_cs) cudaEventDestroy(c->ev_cs);
     if (c->ev_bs) cudaEventDestroy(c->ev_bs);
     c->ev_bs = nullptr;
@@ -590,24 +594,29 @@ dsea_status dalloc(dsea_ctx* c, T** p, size_t count)
     return DSEA_OK;
 }
 
-dsea_status alloc_buf(dsea_ctx* c, BufView* B)
+// a slot buffer of `nslots` slots (slice j in slot j % nslots); the per-cell counters
+// stay per slice (4 B per cell)
+dsea_status alloc_buf(dsea_ctx* c, BufView* B, int nslots, int perm_slots)
 {
     dsea_status s;
     B->L = c->L;
-    if ((s = dalloc(c, &B->base, c->L.slot_bytes * (size_t)c->g.ns))) return s;
+    B->nslots = nslots;
+    B->perm_slots = perm_slots;
+    if ((s = dalloc(c, &B->base, c->L.slot_bytes * (size_t)nslots))) return s;
     if ((s = dalloc(c, &B->cnt, (size_t)c->g.ns * c->g.ncell))) return s;
-    if ((s = dalloc(c, &B->perm, (size_t)c->g.ns * c->g.cap))) return s;
+    if ((s = dalloc(c, &B->perm, (size_t)perm_slots * c->g.cap))) return s;
     CUDA_TRY(c, cudaMemset(B->cnt, 0, sizeof(int32_t) * (size_t)c->g.ns * c->g.ncell));
     // zeroed scratch: after a reported error no later pass can index out of bounds
-    CUDA_TRY(c, cudaMemset(B->perm, 0, sizeof(BinRec) * (size_t)c->g.ns * c->g.cap));
-    CUDA_TRY(c, cudaMemset(B->base, 0, c->L.slot_bytes * (size_t)c->g.ns));
+    CUDA_TRY(c, cudaMemset(B->perm, 0, sizeof(BinRec) * (size_t)perm_slots * c->g.cap));
+    CUDA_TRY(c, cudaMemset(B->base, 0, c->L.slot_bytes * (size_t)nslots));
     return DSEA_OK;
 }
 
 dsea_status alloc_stg(dsea_ctx* c, StgView* S)
 {
     dsea_status s;
-    const size_t n = (size_t)c->g.ns * c->g.cap;
+    S->pool = c->stg_pool;
+    const size_t n = (size_t)c->stg_pool * c->g.cap;
     double** d[] = {&S->x, &S->y, &S->z, &S->vx, &S->vy, &S->vz, &S->fx, &S->fy, &S->fz};
     for (auto* p : d)
         if ((s = dalloc(c, p, n))) return s;
@@ -640,39 +649,98 @@ dsea_status check_dev_err(dsea_ctx* c)
     }
 }
 
-// Bin the flat host state (by id) into the slots of the input buffer.
-dsea_status ensure_aos(dsea_ctx* c)
+// by-id AoS scratch of at least `doubles` doubles
+dsea_status ensure_aos(dsea_ctx* c, size_t doubles)
 {
-    if (c->aos_dev) return DSEA_OK;
     dsea_status s;
-    if ((s = dalloc(c, &c->aos_dev, (size_t)9 * c->N))) return s;
-    if ((s = dalloc(c, &c->count_dev, 1))) return s;
+    if (!c->count_dev && (s = dalloc(c, &c->count_dev, 1))) return s;
+    if (c->aos_cap >= doubles) return DSEA_OK;
+    if (c->aos_dev) {
+        cudaFree(c->aos_dev);
+        c->dallocs.erase(std::remove(c->dallocs.begin(), c->dallocs.end(), (void*)c->aos_dev), c->dallocs.end());
+        c->aos_dev = nullptr;
+        c->aos_cap = 0;
+    }
+    if ((s = dalloc(c, &c->aos_dev, doubles))) return s;
+    c->aos_cap = doubles;
     return DSEA_OK;
 }
 
+// Bin the flat host state (by id) into the slots of the input buffer.  The atoms are
+// grouped on the host by destination slice (the same IEEE floor(x / l_x) as the
+// device, Q4) into runs of slices whose atoms fit the staging buffer (a pool of
+// stg_pool slices on a ring), and each group is uploaded and binned on its own; the
+// slot contents do not depend on the grouping (cells are ordered by (z, id), Q21).
 dsea_status upload_state(dsea_ctx* c, const double* xyz, const double* v, const double* f)
 {
-    // contiguous copies of the caller's by-id arrays; the AoS -> SoA split runs on the GPU
     const int64_t N = c->N;
+    const int ns = c->g.ns;
+    const size_t stg_cap = (size_t)c->stg_pool * c->g.cap;     // flat staging entries
     dsea_status s;
-    if ((s = ensure_aos(c))) return s;
-    double* dx = c->aos_dev;
-    double* dv = c->aos_dev + 3 * (size_t)N;
-    double* df = c->aos_dev + 6 * (size_t)N;
-    CUDA_TRY(c, cudaMemcpyAsync(dx, xyz, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, c->cs));
-    CUDA_TRY(c, cudaMemcpyAsync(dv, v, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, c->cs));
-    if (f) CUDA_TRY(c, cudaMemcpyAsync(df, f, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, c->cs));
-    StgView& S = c->stg[0];
-    aos_to_stage_launch(S, dx, dv, f ? df : nullptr, (int)N, c->cs);
-    c->stats.kernel_launches++;
-    init_keys_launch(c->g, S, (int)N, c->inb.cnt, c->err_dev, c->cs);
-    bin_scan_launch(c->g, c->inb, 0, c->g.ns, c->err_dev, c->cs);
-    bin_place_launch(c->g, c->inb, S, 0, 0, (int)N, 0, c->g.ns, c->err_dev, c->cs);
-    bin_gather_launch(c->g, c->inb, S, 0, c->g.ns, c->err_dev, c->cs);
-    c->stats.kernel_launches += 4;
-    CUDA_TRY(c, cudaStreamSynchronize(c->cs));
-    CUDA_TRY(c, cudaGetLastError());
-    if ((s = check_dev_err(c))) return s;
+    std::vector<int32_t> slice_of((size_t)N);
+    std::vector<int64_t> count((size_t)ns + 1, 0);
+    for (int64_t i = 0; i < N; i++) {
+        const double q = std::floor(xyz[3 * i] / c->g.l[0]);   // reading Q4 (IEEE division)
+        const int cx = !(q >= 0.0) ? 0 : (q >= (double)(c->g.cells[0] - 1) ? c->g.cells[0] - 1 : (int)q);
+        slice_of[(size_t)i] = cx / c->g.c;
+        count[(size_t)slice_of[(size_t)i] + 1]++;
+    }
+    for (int j = 0; j < ns; j++) count[(size_t)j + 1] += count[(size_t)j];
+    // atom ids sorted by slice, id order within a slice (stable counting sort)
+    std::vector<int32_t> order((size_t)N);
+    {
+        std::vector<int64_t> cur(count.begin(), count.end() - 1);
+        for (int64_t i = 0; i < N; i++) order[(size_t)cur[(size_t)slice_of[(size_t)i]]++] = (int32_t)i;
+    }
+    std::vector<int32_t>().swap(slice_of);
+    size_t max_group = 0;
+    for (int m0 = 0; m0 < ns;) {   // largest group that fits the staging buffer
+        int m1 = m0 + 1;
+        while (m1 < ns && (size_t)(count[(size_t)m1 + 1] - count[(size_t)m0]) <= stg_cap) m1++;
+        const size_t na = (size_t)(count[(size_t)m1] - count[(size_t)m0]);
+        if (na > stg_cap)
+            return fail(c, DSEA_ECAPACITY, "slice %d holds %zu atoms (staging capacity %zu)", m0, na, stg_cap);
+        max_group = std::max(max_group, na);
+        m0 = m1;
+    }
+    if ((s = ensure_aos(c, std::max<size_t>(9 * max_group, 1)))) return s;
+    if (!c->ids_dev && (s = dalloc(c, &c->ids_dev, std::max<size_t>(stg_cap, 1)))) return s;
+    std::vector<double> hx, hv, hf;
+    for (int m0 = 0; m0 < ns;) {
+        int m1 = m0 + 1;
+        while (m1 < ns && (size_t)(count[(size_t)m1 + 1] - count[(size_t)m0]) <= stg_cap) m1++;
+        const int64_t a0 = count[(size_t)m0], na = count[(size_t)m1] - a0;
+        if (na > 0) {
+            hx.resize((size_t)na * 3); hv.resize((size_t)na * 3); hf.resize((size_t)na * 3);
+            for (int64_t k = 0; k < na; k++) {
+                const int64_t id = order[(size_t)(a0 + k)];
+                for (int d = 0; d < 3; d++) {
+                    hx[(size_t)(3 * k + d)] = xyz[3 * id + d];
+                    hv[(size_t)(3 * k + d)] = v[3 * id + d];
+                    hf[(size_t)(3 * k + d)] = f ? f[3 * id + d] : 0.0;   // F_new = F_old = 0 (Q7)
+                }
+            }
+            double* dx = c->aos_dev;
+            double* dv = c->aos_dev + 3 * (size_t)na;
+            double* df = c->aos_dev + 6 * (size_t)na;
+            CUDA_TRY(c, cudaMemcpyAsync(dx, hx.data(), sizeof(double) * 3 * na, cudaMemcpyHostToDevice, c->cs));
+            CUDA_TRY(c, cudaMemcpyAsync(dv, hv.data(), sizeof(double) * 3 * na, cudaMemcpyHostToDevice, c->cs));
+            CUDA_TRY(c, cudaMemcpyAsync(df, hf.data(), sizeof(double) * 3 * na, cudaMemcpyHostToDevice, c->cs));
+            CUDA_TRY(c, cudaMemcpyAsync(c->ids_dev, order.data() + a0, sizeof(int32_t) * na, cudaMemcpyHostToDevice,
+                                        c->cs));
+            StgView& S = c->stg[0];
+            aos_to_stage_launch(S, dx, dv, df, c->ids_dev, (int)na, c->cs);
+            init_keys_launch(c->g, S, (int)na, c->inb.cnt, c->err_dev, c->cs);
+        }
+        bin_scan_launch(c->g, c->inb, m0, m1 - m0, c->err_dev, c->cs);
+        if (na > 0) bin_place_launch(c->g, c->inb, c->stg[0], 0, 0, (int)na, m0, m1 - m0, c->err_dev, c->cs);
+        bin_gather_launch(c->g, c->inb, c->stg[0], m0, m1 - m0, c->err_dev, c->cs);
+        c->stats.kernel_launches += na > 0 ? 5 : 2;
+        CUDA_TRY(c, cudaStreamSynchronize(c->cs));   // the host group buffers are reused
+        CUDA_TRY(c, cudaGetLastError());
+        if ((s = check_dev_err(c))) return s;
+        m0 = m1;
+    }
     c->holds_state = true;
     c->mirror_valid = false;
     return DSEA_OK;
@@ -702,18 +770,38 @@ void for_each_atom(dsea_ctx* c, F fn)
     }
 }
 
+// the host start state: FCC lattice (Q10) and velocities (Q9) by id; F = 0 (Q7,
+// implicit: h_f stays empty until a caller sets forces)
+dsea_status ensure_host_state(dsea_ctx* c)
+{
+    if (!c->h_xyz.empty()) return DSEA_OK;
+    try {
+        c->h_xyz.resize((size_t)c->N * 3);
+        c->h_v.resize((size_t)c->N * 3);
+    } catch (...) {
+        c->h_xyz.clear(); c->h_v.clear();
+        return fail(c, DSEA_ENOMEM, "host start state of %lld atoms", (long long)c->N);
+    }
+    host_lattice(c->box, c->a, c->h_xyz.data());
+    host_velocities(c->N, c->box.seed, c->box.T0, c->h_v.data());
+    return DSEA_OK;
+}
+
 dsea_status get_vec(dsea_ctx* c, double* out, int64_t n, int which)
 {
     if (!c) return DSEA_EINVAL;
     if (!out || n != c->N) return fail(c, DSEA_EINVAL, "array of %lld atoms expected", (long long)c->N);
     if (!c->sliced) {
+        dsea_status s = ensure_host_state(c);
+        if (s) return s;
         const std::vector<double>& src = which == 0 ? c->h_xyz : which == 1 ? c->h_v : c->h_f;
-        std::memcpy(out, src.data(), sizeof(double) * 3 * (size_t)c->N);
+        if (src.empty()) std::memset(out, 0, sizeof(double) * 3 * (size_t)c->N);   // forces: 0 (Q7)
+        else std::memcpy(out, src.data(), sizeof(double) * 3 * (size_t)c->N);
         return DSEA_OK;
     }
     if (!c->holds_state) return fail(c, DSEA_ESTATE, "this rank does not hold the state (rank 0 does)");
     // scatter by id on the GPU, then one contiguous device-to-host copy
-    dsea_status s = ensure_aos(c);
+    dsea_status s = ensure_aos(c, 3 * (size_t)c->N);
     if (s) return s;
     CUDA_TRY(c, cudaSetDevice(c->device));
     CUDA_TRY(c, cudaMemsetAsync(c->count_dev, 0, sizeof(unsigned long long), c->cs));
@@ -748,6 +836,40 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
     NcclApi& api = nccl();
     const int W = c->W;
     auto in_of = [&](int w) -> BufView& { return w == 0 ? c->inb : c->outb[w - 1]; };
+    // copy slices [j, j+n) between slot buffers of dst_slots / src_slots slots (slice s in
+    // slot s % slots): one cudaMemcpyAsync per run that wraps around neither buffer
+    auto copy_run = [&](char* dst, int dst_slots, const char* src, int src_slots, int j, int n,
+                        cudaStream_t st) -> dsea_status {
+        for (int k = 0; k < n;) {
+            const int sd = (j + k) % dst_slots, ss_ = (j + k) % src_slots;
+            const int run = std::min(n - k, std::min(dst_slots - sd, src_slots - ss_));
+            CUDA_TRY(c, cudaMemcpyAsync(dst + (size_t)sd * sb, src + (size_t)ss_ * sb, sb * run,
+                                        cudaMemcpyDeviceToDevice, st));
+            k += run;
+        }
+        return DSEA_OK;
+    };
+    // the last worker's output pool: before slices [m, m+n) are written into it, the
+    // hops that read the previous occupants of those slots must be done
+    auto wait_pool = [&](int m, int n, cudaStream_t st) -> dsea_status {
+        BufView& ob = c->outb[W - 1];
+        for (int sl = m; sl < m + n; sl++) {
+            const int p = sl % ob.nslots;
+            if (p < (int)c->pslot_rec.size() && c->pslot_rec[(size_t)p])
+                CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_pslot[(size_t)p], 0));
+        }
+        return DSEA_OK;
+    };
+    auto record_pool = [&](int m, int n, cudaStream_t st) -> dsea_status {
+        BufView& ob = c->outb[W - 1];
+        for (int sl = m; sl < m + n; sl++) {
+            const int p = sl % ob.nslots;
+            if (p >= (int)c->pslot_rec.size()) continue;
+            CUDA_TRY(c, cudaEventRecord(c->ev_pslot[(size_t)p], st));
+            c->pslot_rec[(size_t)p] = 1;
+        }
+        return DSEA_OK;
+    };
     // counter mode (c->ctr): event number of the k-th arrival / release of slot s
     auto ev_no = [&](uint32_t k, int s) { return (k - 1) * (uint32_t)ns + (uint32_t)s + 1; };
     auto wait_arrival = [&](int s) -> dsea_status {
@@ -903,10 +1025,17 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 }
             }
             BufView& src = in_of(w);
-            char* dst_base = (c->ce_hop && w == W - 1 && c->NG > 1) ? c->succ_in_base : c->outb[w].base;
-            if (src.base != dst_base)
-                CUDA_TRY(c, cudaMemcpyAsync(dst_base + (size_t)j * sb, src.base + (size_t)j * sb, sb * n,
-                                            cudaMemcpyDeviceToDevice, c->cs));
+            const bool to_succ = c->ce_hop && w == W - 1 && c->NG > 1;
+            char* dst_base = to_succ ? c->succ_in_base : c->outb[w].base;
+            const int dst_slots = to_succ ? ns : c->outb[w].nslots;
+            if (!to_succ && w == W - 1 && c->NG > 1) {
+                dsea_status s = wait_pool(j, n, c->cs);
+                if (s) return s;
+            }
+            if (src.base != dst_base) {
+                dsea_status s = copy_run(dst_base, dst_slots, src.base, src.nslots, j, n, c->cs);
+                if (s) return s;
+            }
             if (w == 0 && c->NG > 1) {
                 if (c->peer) {
                     const uint32_t v = ++c->rel_cnt[j];
@@ -930,8 +1059,10 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 // the successor's arrival flags -- neither needs an SM, so both overlap
                 // the next block's (persistent, SM-filling) force pass
                 const int nblk = c->bl.n();
-                for (int k = c->bl.of[m]; k <= c->bl.of[m + n - 1]; k++)   // previous push of these slots
-                    if (c->hop_rec[k]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_hop[k], 0));
+                {   // the pushes that read the previous occupants of these pool slots
+                    dsea_status s = wait_pool(m, n, c->cs);
+                    if (s) return s;
+                }
                 (void)nblk;
                 cudaEvent_t t0 = nullptr, t1 = nullptr;
                 if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
@@ -958,8 +1089,10 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 }
                 cudaEvent_t h0 = nullptr, h1 = nullptr;
                 if (c->timing) { h0 = tev(c); h1 = tev(c); cudaEventRecord(h0, c->bs); }
-                CUDA_TRY(c, cudaMemcpyAsync(c->succ_in_base + (size_t)m * sb, ob.base + (size_t)m * sb, sb * n,
-                                            cudaMemcpyDeviceToDevice, c->bs));
+                {
+                    dsea_status s = copy_run(c->succ_in_base, ns, ob.base, ob.nslots, m, n, c->bs);
+                    if (s) return s;
+                }
                 if (c->ctr) {
                     if (stream_write32(c->bs, c->succ_arr, ev_no(c->push_k[m + n - 1], m + n - 1)))
                         return fail(c, DSEA_EPEER, "cuStreamWriteValue32 (arrival) failed");
@@ -970,9 +1103,10 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                             return fail(c, DSEA_EPEER, "cuStreamWriteValue32 (arrival) failed");
                 }
                 if (c->timing) { cudaEventRecord(h1, c->bs); c->tpairs.push_back({TK_SEND, {h0, h1}}); }
-                const int key = c->bl.of[m + n - 1] % nblk;
-                CUDA_TRY(c, cudaEventRecord(c->ev_hop[key], c->bs));
-                c->hop_rec[key] = 1;
+                {
+                    dsea_status s = record_pool(m, n, c->bs);
+                    if (s) return s;
+                }
                 c->stats.hop_bytes += (int64_t)sb * n;
                 break;
             }
@@ -995,6 +1129,8 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 } else {
                     for (int sl = m; sl < m + n; sl++)
                         if (sent[sl]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[sl], 0));
+                    dsea_status s = wait_pool(m, n, c->cs);
+                    if (s) return s;
                 }
             }
             cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -1031,7 +1167,8 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->ss); }
             api.GroupStart();
             for (size_t q = oi; q < oe; q++) {
-                ncclResult_t r = api.Send(c->outb[W - 1].base + (size_t)ops[q].slice * sb, sb, ncclChar, 1,
+                const BufView& ob = c->outb[W - 1];
+                ncclResult_t r = api.Send(ob.base + (size_t)(ops[q].slice % ob.nslots) * sb, sb, ncclChar, 1,
                                           c->send_comm, c->ss);
                 if (r != ncclSuccess) { api.GroupEnd(); return fail(c, DSEA_EPEER, "ncclSend: %s", api.GetErrorString(r)); }
             }
@@ -1042,6 +1179,8 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 CUDA_TRY(c, cudaEventRecord(c->ev_send[ops[q].slice], c->ss));
                 sent[ops[q].slice] = 1;
                 c->stats.hop_bytes += (int64_t)sb;
+                dsea_status s = record_pool(ops[q].slice, 1, c->ss);
+                if (s) return s;
             }
             oi = oe - 1;
             break;
@@ -1122,16 +1261,9 @@ dsea_status dsea_init(const dsea_box_params* box, dsea_ctx** out)
     c->b[1] = box->ny * c->a;
     c->b[2] = box->nz * c->a;
     c->N = N;
-    try {
-        c->h_xyz.resize((size_t)N * 3);
-        c->h_v.resize((size_t)N * 3);
-        c->h_f.assign((size_t)N * 3, 0.0);  // F_new = F_old = 0 at start (Q7)
-    } catch (...) {
-        delete c;
-        return DSEA_ENOMEM;
-    }
-    host_lattice(*box, c->a, c->h_xyz.data());
-    host_velocities(N, box->seed, box->T0, c->h_v.data());
+    // the start state (FCC lattice + velocities by id) is generated on first use: only
+    // the rank that uploads it (rank 0 of a ring) ever materialises the 48 B/atom host
+    // arrays (at 1e9 atoms every other rank would otherwise hold 48 GB it never reads)
     *out = c;
     return DSEA_OK;
 }
@@ -1194,9 +1326,11 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
         if ((s = get_vec(c, xyz.data(), c->N, 0)) || (s = get_vec(c, v.data(), c->N, 1)) ||
             (s = get_vec(c, f.data(), c->N, 2)))
             return s;
-    } else if (!c->sliced) {
-        xyz = c->h_xyz; v = c->h_v; f = c->h_f;
     }
+    // the host start state (never sliced yet) moves into the device slots of the
+    // uploading rank; the host copy is released once the upload succeeded
+    const bool from_host = !c->sliced && (sp->rank == 0 || sp->n_gpus == 1);
+    if (from_host && (s = ensure_host_state(c))) return s;
     free_device(c);
 
     c->sp = *sp;
@@ -1258,14 +1392,36 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     c->prof.assign((size_t)c->g.ns, dsea_profile{});
 
     // buffers: input buffer + one output buffer per worker; the last worker of a ring
-    // of one writes straight back into the input buffer (local hand-off).
-    if ((s = alloc_buf(c, &c->inb))) return s;
+    // of one writes straight back into the input buffer (local hand-off).  On the staged
+    // schedule only a window of slices is live in a worker's staging buffer (a block's
+    // pass writes B slices; the pending bins read one slice on each side) and in the
+    // last worker's local output buffer of a ring (binned, then pushed or sent): pools
+    // of stg_pool / out_pool slots (slice j in slot j % pool, P:121-122's circular
+    // slot buffers, NEXT-3).  The input buffer keeps N_S slots: rank 0 holds the whole
+    // state between calls (Q22).
+    {
+        int bmax = 1;
+        for (int k = 0; k < c->bl.n(); k++) bmax = std::max(bmax, c->bl.count(k));
+        const bool staged = mode == DSEA_MODE_STAGED;
+        c->stg_pool = (staged && c->T.kind == FORCE_TILE) ? std::min(g.ns, 2 * bmax + 4) : g.ns;
+        const char* hop = getenv("DSEA_PEER_HOP");
+        const bool sm_hop = hop && std::strcmp(hop, "sm") == 0;   // remote stores need the full buffer
+        c->out_pool = (c->NG > 1 && !sm_hop) ? std::min(g.ns, 4 * bmax + 4) : g.ns;
+        if (const char* e = getenv("DSEA_FULL_POOLS"); e && *e && atoi(e) != 0) c->stg_pool = c->out_pool = g.ns;
+    }
+    // the input buffer is binned into only by the fused pass / a ring of one (all slices
+    // at once) and by the upload (groups of <= stg_pool slices)
+    if ((s = alloc_buf(c, &c->inb, g.ns, c->NG == 1 ? g.ns : c->stg_pool))) return s;
     c->outb.resize(c->W);
     for (int w = 0; w < c->W; w++) {
         const bool alias = (w == c->W - 1) && c->NG == 1;
+        const int np = w == c->W - 1 ? c->out_pool : g.ns;
         if (alias) c->outb[w] = c->inb;
-        else if ((s = alloc_buf(c, &c->outb[w]))) return s;
+        else if ((s = alloc_buf(c, &c->outb[w], np, np))) return s;
     }
+    c->ev_pslot.resize((size_t)c->out_pool);
+    for (auto& e : c->ev_pslot) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->pslot_rec.assign((size_t)c->out_pool, 0);
     c->stg.resize(c->W);
     for (int w = 0; w < c->W; w++)
         if ((s = alloc_stg(c, &c->stg[w]))) return s;
@@ -1284,9 +1440,6 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
         const int nblk = c->bl.n();
         c->ev_binblk.resize(nblk);
         for (int k = 0; k < nblk; k++) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_binblk[k], cudaEventDisableTiming));
-        c->ev_hop.resize(nblk);
-        for (int k = 0; k < nblk; k++) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_hop[k], cudaEventDisableTiming));
-        c->hop_rec.assign(nblk, 0);
     }
     c->ev_force.resize(c->W);
     for (int w = 0; w < c->W; w++) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_force[w], cudaEventDisableTiming));
@@ -1301,8 +1454,16 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
     if (c->NG > geo.n_max)
         c->msg = "note: N_GPU exceeds N_max of Eq. (1); the ring runs at the plateau (P:364)";
     if (c->rank == 0 || c->NG == 1) {
-        if (xyz.empty()) return fail(c, DSEA_ESTATE, "no state to slice");
-        if ((s = upload_state(c, xyz.data(), v.data(), f.data()))) return s;
+        const std::vector<double>& X = from_host ? c->h_xyz : xyz;
+        const std::vector<double>& V = from_host ? c->h_v : v;
+        const std::vector<double>& F = from_host ? c->h_f : f;
+        if (X.empty()) return fail(c, DSEA_ESTATE, "no state to slice");
+        if ((s = upload_state(c, X.data(), V.data(), F.empty() ? nullptr : F.data()))) return s;
+        if (from_host) {
+            std::vector<double>().swap(c->h_xyz);
+            std::vector<double>().swap(c->h_v);
+            std::vector<double>().swap(c->h_f);
+        }
     }
     return DSEA_OK;
 }
@@ -1438,7 +1599,7 @@ dsea_status dsea_ring_connect_peer(dsea_ctx* c, const void* blobs, size_t blob_b
         last.base = c->succ_in_base;
         last.remote = 1;
     }
-    std::fill(c->hop_rec.begin(), c->hop_rec.end(), 0);
+    std::fill(c->pslot_rec.begin(), c->pslot_rec.end(), 0);
     CUDA_TRY(c, cudaDeviceSynchronize());
     c->connected = true;
     return DSEA_OK;
@@ -1620,6 +1781,37 @@ dsea_status dsea_get_cells(dsea_ctx* c, int32_t* cell_xyz, int32_t* slice, int64
     return DSEA_OK;
 }
 
+dsea_status dsea_get_slice(dsea_ctx* c, int32_t j, double* xyz, double* v, double* f, int32_t* ids, int64_t cap,
+                           int64_t* n_written)
+{
+    if (!c || !n_written) return DSEA_EINVAL;
+    if (!c->sliced) return fail(c, DSEA_ESTATE, "dsea_get_slice before dsea_slice");
+    if (j < 0 || j >= c->g.ns) return fail(c, DSEA_EINVAL, "slice %d outside [0, %d)", j, c->g.ns);
+    if (!c->holds_state) return fail(c, DSEA_ESTATE, "this rank does not hold the state (rank 0 does)");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    const char* slot = c->inb.base + (size_t)(j % c->inb.nslots) * c->L.slot_bytes;
+    int32_t n = 0;
+    CUDA_TRY(c, cudaMemcpy(&n, slot + sizeof(int32_t) * (size_t)c->g.ncell, sizeof n, cudaMemcpyDeviceToHost));
+    *n_written = n;
+    const int64_t k = std::min<int64_t>(cap, n);
+    if (k <= 0) return DSEA_OK;
+    std::vector<double> a((size_t)k), b((size_t)k), d((size_t)k);
+    auto aos = [&](double* out, size_t ox, size_t oy, size_t oz) -> dsea_status {
+        if (!out) return DSEA_OK;
+        CUDA_TRY(c, cudaMemcpy(a.data(), slot + ox, sizeof(double) * k, cudaMemcpyDeviceToHost));
+        CUDA_TRY(c, cudaMemcpy(b.data(), slot + oy, sizeof(double) * k, cudaMemcpyDeviceToHost));
+        CUDA_TRY(c, cudaMemcpy(d.data(), slot + oz, sizeof(double) * k, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < k; i++) { out[3 * i] = a[(size_t)i]; out[3 * i + 1] = b[(size_t)i]; out[3 * i + 2] = d[(size_t)i]; }
+        return DSEA_OK;
+    };
+    dsea_status s;
+    if ((s = aos(xyz, c->L.off_x, c->L.off_y, c->L.off_z))) return s;
+    if ((s = aos(v, c->L.off_vx, c->L.off_vy, c->L.off_vz))) return s;
+    if ((s = aos(f, c->L.off_fx, c->L.off_fy, c->L.off_fz))) return s;
+    if (ids) CUDA_TRY(c, cudaMemcpy(ids, slot + c->L.off_id, sizeof(int32_t) * k, cudaMemcpyDeviceToHost));
+    return DSEA_OK;
+}
+
 dsea_status dsea_set_thermostat(dsea_ctx* c, int32_t enable, double T_target)
 {
     if (!c) return DSEA_EINVAL;
@@ -1699,10 +1891,10 @@ dsea_status dsea_set_state(dsea_ctx* c, const double* xyz, const double* v, cons
     if (!c) return DSEA_EINVAL;
     if (!xyz || !v || n != c->N) return fail(c, DSEA_EINVAL, "positions and velocities of %lld atoms expected", (long long)c->N);
     if (!c->sliced) {
-        std::memcpy(c->h_xyz.data(), xyz, sizeof(double) * 3 * n);
-        std::memcpy(c->h_v.data(), v, sizeof(double) * 3 * n);
-        if (f) std::memcpy(c->h_f.data(), f, sizeof(double) * 3 * n);
-        else std::fill(c->h_f.begin(), c->h_f.end(), 0.0);
+        c->h_xyz.assign(xyz, xyz + 3 * n);
+        c->h_v.assign(v, v + 3 * n);
+        if (f) c->h_f.assign(f, f + 3 * n);
+        else c->h_f.clear();
         return DSEA_OK;
     }
     if (c->NG > 1 && c->rank != 0) return DSEA_OK;

@@ -70,15 +70,21 @@ struct BinRec {
 struct BufView {
     char* base;
     SlotLayout L;
-    int32_t* cnt;    // [ns*ncell] per-cell arrival counters / cursors (not sent)
-    BinRec* perm;    // [ns*cap] bin scratch (not sent)
+    int32_t* cnt;    // [ns*ncell] per-cell arrival counters / cursors, by slice (not sent)
+    BinRec* perm;    // [nslots*cap] bin scratch, by slot (not sent)
     int remote;      // slots live in the ring successor's memory (peer backend)
+    int nslots;      // slots of the buffer: slice j lives in slot j % nslots (a pool of
+                     // nslots < ns slots when only a window of slices is ever live,
+                     // P:121-122 "s slots", s N_b > N_S; NEXT-3)
+    int perm_slots;  // slots of the bin scratch: slice m uses perm[(m % perm_slots) * cap ..]
 };
 
 // Device view of a staging buffer (flat SoA over ns*cap entries).
 struct StgView {
+    // staged atom i of slice j at index (j % pool) * cap + i (a pool of `pool` slices)
     double *x, *y, *z, *vx, *vy, *vz, *fx, *fy, *fz;
     int32_t *id, *key;
+    int pool;        // slices the arrays hold (ns in the fused pass; a window on a ring)
     int32_t* n;      // [ns] atoms staged per slice
     double4* eatom;  // energy records (u_core, vir2, ke2, pairs) of the last force pass:
                      // FORCE_TILE one per tile [ns*tiles], FORCE_PIPE one per atom [ns*cap]
@@ -134,7 +140,9 @@ Tiling pipe_tiling(const Geo& g, double mean_per_cell, int smem_optin);
 int pipe_kernel_attr(const Tiling& T);
 void pipe_launch(const Geo& g, const Tiling& T, BufView in, StgView stg, int32_t* out_cnt, int j0, int nj,
                  DevErr* err, cudaStream_t s);
-void aos_to_stage_launch(StgView S, const double* xyz, const double* v, const double* f, int n, cudaStream_t s);
+// flat staging [0, n) from by-atom AoS arrays; ids: the atoms' ids (nullptr: 0..n-1)
+void aos_to_stage_launch(StgView S, const double* xyz, const double* v, const double* f, const int32_t* ids,
+                         int n, cudaStream_t s);
 void slots_to_aos_launch(const Geo& g, BufView in, int which, double* out, unsigned long long* count,
                          cudaStream_t s);
 void signal_launch(uint32_t* flags, int first, int n, uint32_t value, cudaStream_t s);

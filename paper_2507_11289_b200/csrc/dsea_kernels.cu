@@ -483,7 +483,7 @@ k_force_pipe(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
                 const double vy = vy0 + (Fy + fyo) * hdt;
                 const double vz = vz0 + (Fz + fzo) * hdt;
                 const double ke2 = vx * vx + vy * vy + vz * vz;
-                const size_t st = (size_t)j * g.cap + gi;
+                const size_t st = stg_index(stg, j, g.cap, gi);
                 stg.eatom[st] = make_double4(e_u, e_v, ke2, (double)e_np);
                 if (NVT) {
                     // NVT: the slice's scale factor needs every atom's kick first
@@ -560,7 +560,7 @@ k_drift(Geo g, StgView stg, int j0, const UnitEnergy* __restrict__ e_out, int32_
     const int n = stg.n[j];
     const double lam = e_out[j].lambda;
     for (int i = blockIdx.x * DRIFT_THREADS + threadIdx.x; i < n; i += gridDim.x * DRIFT_THREADS) {
-        const size_t st = (size_t)j * g.cap + i;
+        const size_t st = stg_index(stg, j, g.cap, i);
         drift_store(g, stg, st, j, stg.x[st], stg.y[st], stg.z[st], lam * stg.vx[st], lam * stg.vy[st],
                     lam * stg.vz[st], stg.fx[st], stg.fy[st], stg.fz[st], stg.id[st], out_cnt, err);
     }
@@ -650,7 +650,7 @@ k_bin_place(Geo g, BufView out, StgView stg, int s0, int flat_count, int m0, int
     pdl_release();
     int base, n;
     if (flat_count > 0) { base = 0; n = flat_count; }
-    else { const int s = s0 + blockIdx.y; base = s * g.cap; n = stg.n[s]; }
+    else { const int s = s0 + blockIdx.y; base = (s % stg.pool) * g.cap; n = stg.n[s]; }
     const int p = blockIdx.x * PLACE_THREADS + threadIdx.x;
     if (p >= n) return;
     const int key = stg.key[base + p];
@@ -666,7 +666,7 @@ k_bin_place(Geo g, BufView out, StgView stg, int s0, int flat_count, int m0, int
         r.z = stg.z[base + p];
         r.src = base + p;
         r.id = stg.id[base + p];
-        out.perm[(size_t)m * g.cap + pos] = r;
+        out.perm[(size_t)(m % out.perm_slots) * g.cap + pos] = r;
     }
 }
 
@@ -700,7 +700,7 @@ k_bin_gather(Geo g, BufView out, StgView stg, int m0)
     if (sub == 0) out.cnt[(size_t)m * g.ncell + c] = 0;
     if (cs[g.ncell] > g.cap) return;  // capacity error already flagged by the scan
     const int n = en - st;
-    const BinRec* R = out.perm + (size_t)m * g.cap + st;
+    const BinRec* R = out.perm + (size_t)(m % out.perm_slots) * g.cap + st;
     double* ox = slot_d(out, m, out.L.off_x);
     double* oy = slot_d(out, m, out.L.off_y);
     double* oz = slot_d(out, m, out.L.off_z);
@@ -778,7 +778,7 @@ __global__ void k_init_keys(Geo g, StgView stg, int n, int32_t* __restrict__ out
 // host only issues contiguous copies.
 // ------------------------------------------------------------------------------
 __global__ void k_aos_to_stage(StgView S, const double* __restrict__ xyz, const double* __restrict__ v,
-                               const double* __restrict__ f, int n)
+                               const double* __restrict__ f, const int32_t* __restrict__ ids, int n)
 {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
@@ -786,7 +786,7 @@ __global__ void k_aos_to_stage(StgView S, const double* __restrict__ xyz, const 
     S.vx[p] = v[3 * (size_t)p]; S.vy[p] = v[3 * (size_t)p + 1]; S.vz[p] = v[3 * (size_t)p + 2];
     if (f) { S.fx[p] = f[3 * (size_t)p]; S.fy[p] = f[3 * (size_t)p + 1]; S.fz[p] = f[3 * (size_t)p + 2]; }
     else { S.fx[p] = 0.0; S.fy[p] = 0.0; S.fz[p] = 0.0; }
-    S.id[p] = p;
+    S.id[p] = ids ? ids[p] : p;
 }
 
 __global__ void k_slots_to_aos(Geo g, BufView in, int which, double* __restrict__ out,
@@ -809,9 +809,10 @@ __global__ void k_slots_to_aos(Geo g, BufView in, int which, double* __restrict_
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, (unsigned long long)__popc(b));
 }
 
-void aos_to_stage_launch(StgView S, const double* xyz, const double* v, const double* f, int n, cudaStream_t s)
+void aos_to_stage_launch(StgView S, const double* xyz, const double* v, const double* f, const int32_t* ids,
+                         int n, cudaStream_t s)
 {
-    k_aos_to_stage<<<(n + 255) / 256, 256, 0, s>>>(S, xyz, v, f, n);
+    k_aos_to_stage<<<(n + 255) / 256, 256, 0, s>>>(S, xyz, v, f, ids, n);
 }
 
 void slots_to_aos_launch(const Geo& g, BufView in, int which, double* out, unsigned long long* count,

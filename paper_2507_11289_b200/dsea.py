@@ -109,6 +109,7 @@ SIGNATURES = [
     ("dsea_get_forces", _st, [_c, _pd, ctypes.c_int64]),
     ("dsea_get_cells", _st, [_c, _pi32, _pi32, ctypes.c_int64]),
     ("dsea_get_energies", _st, [_c, ctypes.POINTER(dsea_energy), ctypes.c_int64, _pi64]),
+    ("dsea_get_slice", _st, [_c, ctypes.c_int32, _pd, _pd, _pd, _pi32, ctypes.c_int64, _pi64]),
     ("dsea_set_state", _st, [_c, _pd, _pd, _pd, ctypes.c_int64]),
     ("dsea_set_thermostat", _st, [_c, ctypes.c_int32, ctypes.c_double]),
     ("dsea_get_profiles", _st, [_c, ctypes.POINTER(dsea_profile), ctypes.c_int32]),
@@ -338,6 +339,18 @@ def dsea_get_energies(ctx):
     rec = rec[:n.value]
     arr = np.stack([rec["U"], rec["KE"], rec["V"], rec["U"] + rec["KE"]], axis=1) if n.value else np.zeros((0, 4))
     return rec["step"].copy(), arr
+
+
+def dsea_get_slice(ctx, j):
+    """The atoms of slice j in slot order: dict of xyz [n, 3], v [n, 3], f [n, 3], id [n]."""
+    n = ctypes.c_int64()
+    _check(ctx, lib.dsea_get_slice(ctx, int(j), None, None, None, None, 0, ctypes.byref(n)))
+    k = n.value
+    xyz, v, f = np.zeros((k, 3)), np.zeros((k, 3)), np.zeros((k, 3))
+    ids = np.zeros(k, dtype=np.int32)
+    _check(ctx, lib.dsea_get_slice(ctx, int(j), _pd_of(xyz), _pd_of(v), _pd_of(f), ids.ctypes.data_as(_pi32), k,
+                                   ctypes.byref(n)))
+    return {"xyz": xyz, "v": v, "f": f, "id": ids}
 
 
 def dsea_set_thermostat(ctx, T_target):

@@ -473,3 +473,23 @@ def test_first_step_forces_rc4():
     _force_close(e.forces(), Fo, tol=1e-10)
     _, en = e.energies()
     assert np.allclose(en[0, :3], eo[0, :3], rtol=1e-10)
+
+
+def test_get_slice_matches_by_id_readback():
+    """dsea_get_slice (one slot at a time, the read-back for states too large to gather
+    by id): every slice's atoms, ids and vectors equal the by-id arrays; the slices
+    partition the atoms."""
+    e, c = _engine("C1")
+    e.step(3)
+    x, v, f = e.positions(), e.velocities(), e.forces()
+    seen = []
+    for j in range(c.n_slices):
+        s = D.dsea_get_slice(e.ctx, j)
+        assert np.array_equal(s["xyz"], x[s["id"]])
+        assert np.array_equal(s["v"], v[s["id"]])
+        assert np.array_equal(s["f"], f[s["id"]])
+        seen.append(s["id"])
+    ids = np.sort(np.concatenate(seen))
+    assert np.array_equal(ids, np.arange(c.n_atoms))
+    with pytest.raises(D.DseaError):
+        D.dsea_get_slice(e.ctx, c.n_slices)
