@@ -167,18 +167,27 @@ dsea_status dsea_ring_connect(dsea_ctx *ctx, const void *ids, int32_t n_ids);
 /* Write one fresh 128-byte ncclUniqueId into out (out_bytes >= 128). */
 dsea_status dsea_ring_unique_id(void *out, size_t out_bytes);
 
-/* Peer backend (default for bench.py).  The ring hop of P:118-119 is fused into the
- * finalisation of the last worker on each GPU: its bin kernels write the finished
- * slices straight into the successor GPU's input slots over NVLink (CUDA IPC
- * mapping), and arrival / release counts travel through two small flag arrays
- * (receivers wait on local flags with stream memory operations).  No copy, no
- * NCCL kernel on the data path.
- * dsea_ring_export writes this rank's IPC handles (input buffer, flag arrays) into
- * out (cap >= *len; out = NULL queries *len).  dsea_ring_connect_peer takes the
- * n_blobs = n_gpus blobs of all ranks, concatenated in rank order (each blob_bytes
- * long), maps the successor's input buffer and flags and the predecessor's release
- * flags.  Collective: every rank calls it, then the caller must barrier before the
- * first dsea_step.  Exclusive with dsea_ring_connect on a context. */
+/* Peer backend (default for bench.py).  The ring hop of P:118-119 runs on the copy
+ * engines over NVLink (CUDA IPC mapping of the successor's input buffer): the last
+ * worker on each GPU bins its finished slices into a local output pool (slice j in
+ * slot j % pool), then a copy stream pushes them with cudaMemcpyAsync into the
+ * successor's input slots and raises the successor's monotone ARRIVAL counter with
+ * cuStreamWriteValue32; the successor's compute stream waits on that counter
+ * (cuStreamWaitValue32, >=), and its consumption raises the predecessor's monotone
+ * RELEASE counter, which the next push into the same slots waits on.  No SM and no
+ * NCCL kernel is on the data path, so the hop overlaps the next block's force pass.
+ * A/B paths (environment, every rank alike; a mismatch fails connect with
+ * DSEA_EINVAL): DSEA_PEER_HOP=sm (bin kernels store straight into the successor's
+ * slots, full-size buffers), DSEA_RING_COUNTERS=0 (one flag per slot instead of the
+ * two counters).
+ * dsea_ring_export writes this rank's IPC handles (input buffer, counter arrays) and
+ * ring settings into out (cap >= *len; out = NULL queries *len).
+ * dsea_ring_connect_peer takes the n_blobs = n_gpus blobs of all ranks, concatenated
+ * in rank order (each blob_bytes long), checks that every rank runs the same slicing,
+ * W, block partition and hop settings, and maps the successor's input buffer and
+ * arrival counter and the predecessor's release counter.  Collective: every rank
+ * calls it, then the caller must barrier before the first dsea_step.  Exclusive with
+ * dsea_ring_connect on a context. */
 dsea_status dsea_ring_export(dsea_ctx *ctx, void *out, size_t cap, size_t *len);
 dsea_status dsea_ring_connect_peer(dsea_ctx *ctx, const void *blobs, size_t blob_bytes, int32_t n_blobs);
 

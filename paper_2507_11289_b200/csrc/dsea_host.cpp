@@ -269,11 +269,7 @@ Plan build_plan(int ns, int ng, int rank, int W, int64_t n_steps, const Blocks& 
     return P;
 }
 
-// Idle stages between super-cycles.  With W > 1 workers, worker 0 starts super-cycle
-// K+1 while the later workers still finish K; past Eq. (1)'s bound (P:192-195) the
-// data worker 0 waits for from the ring then depends on exactly those trailing
-// blocks, and the stream order would deadlock.  There the ring is at its plateau
-// anyway (P:364): a gap of d (W-1) stages lets every rank finish K first.
+// push order within a stage: see order_pushes in dsea_plan.h
 void order_pushes(std::vector<Op>& ops, int W)
 {
     for (size_t i = 0; i + 1 < ops.size(); i++)
@@ -284,6 +280,11 @@ void order_pushes(std::vector<Op>& ops, int W)
                 if (ops[k].cycle < ops[i].cycle) std::rotate(ops.begin() + i, ops.begin() + k, ops.begin() + k + 1), i++;
 }
 
+// Idle stages between super-cycles.  With W > 1 workers, worker 0 starts super-cycle
+// K+1 while the later workers still finish K; past Eq. (1)'s bound (P:192-195) the
+// data worker 0 waits for from the ring then depends on exactly those trailing
+// blocks, and the stream order would deadlock.  There the ring is at its plateau
+// anyway (P:364): a gap of d (W-1) stages lets every rank finish K first.
 bool plan_plateau(int ng, int W, const Blocks& bl)
 {
     if (ng == 1) return false;
@@ -1058,12 +1059,10 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 // then the copy stream pushes the finished slots over NVLink and raises
                 // the successor's arrival flags -- neither needs an SM, so both overlap
                 // the next block's (persistent, SM-filling) force pass
-                const int nblk = c->bl.n();
                 {   // the pushes that read the previous occupants of these pool slots
                     dsea_status s = wait_pool(m, n, c->cs);
                     if (s) return s;
                 }
-                (void)nblk;
                 cudaEvent_t t0 = nullptr, t1 = nullptr;
                 if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
                 const int s0 = std::max(m - 1, 0), s1 = std::min(m + n, ns - 1);

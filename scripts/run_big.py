@@ -72,8 +72,10 @@ def main():
         import oracle
         rng = np.random.default_rng(7)
         worst = 0.0
+        after = {}
+        for m in before:
+            after[m] = D.dsea_get_slice(e.ctx, m)
         for j in sl:
-            after = D.dsea_get_slice(e.ctx, j)
             nb = [before[m] for m in (j - 1, j, j + 1) if m in before]
             loc = np.concatenate([b["xyz"] for b in nb])
             loc_id = np.concatenate([b["id"] for b in nb])
@@ -83,8 +85,11 @@ def main():
             pos_in_loc = {int(i): k for k, i in enumerate(loc_id)}
             idx = np.array([pos_in_loc[int(own["id"][p])] for p in pick], dtype=np.int64)
             Fo, _ = oracle.forces_subset(loc, g.b, 2.5, idx)
-            fmap = {int(i): k for k, i in enumerate(after["id"])}
-            Fg = np.array([after["f"][fmap[int(own["id"][p])]] for p in pick])
+            # the picked atoms after the step (one may have crossed into a neighbour slice)
+            aid = np.concatenate([after[m]["id"] for m in (j - 1, j, j + 1) if m in after])
+            af = np.concatenate([after[m]["f"] for m in (j - 1, j, j + 1) if m in after])
+            fmap = {int(i): k for k, i in enumerate(aid)}
+            Fg = np.array([af[fmap[int(own["id"][p])]] for p in pick])
             frms = np.sqrt((Fo ** 2).sum(1).mean())
             err = np.sqrt(((Fg - Fo) ** 2).sum(1)) / np.maximum(np.sqrt((Fo ** 2).sum(1)), frms)
             worst = max(worst, float(err.max()))

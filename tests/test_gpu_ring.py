@@ -1,4 +1,6 @@
-"""Multi-GPU ring (one process per GPU, NCCL point-to-point links; §3.1,
+"""Multi-GPU ring (one process per GPU; the hop of P:117-120 §3.1 by the "peer"
+backend -- copy-engine pushes into the successor's IPC-mapped slots with monotone
+arrival / release counters -- or the "nccl" backend's send/recv;
 P:200-208 §3.4): the state after n steps equals the single-GPU run bit for bit --
 the ring is an exact re-scheduling of timesteps and every
 kernel result depends only on its input slots.  Needs >= 2 GPUs (gpurun --gpus N)."""
