@@ -603,6 +603,7 @@ dsea_status alloc_buf(dsea_ctx* c, BufView* B, int nslots, int perm_slots)
     B->L = c->L;
     B->nslots = nslots;
     B->perm_slots = perm_slots;
+    B->soff = 0;
     if ((s = dalloc(c, &B->base, c->L.slot_bytes * (size_t)nslots))) return s;
     if ((s = dalloc(c, &B->cnt, (size_t)c->g.ns * c->g.ncell))) return s;
     if ((s = dalloc(c, &B->perm, (size_t)perm_slots * c->g.cap))) return s;
@@ -617,6 +618,7 @@ dsea_status alloc_stg(dsea_ctx* c, StgView* S)
 {
     dsea_status s;
     S->pool = c->stg_pool;
+    S->soff = 0;
     const size_t n = (size_t)c->stg_pool * c->g.cap;
     double** d[] = {&S->x, &S->y, &S->z, &S->vx, &S->vy, &S->vz, &S->fx, &S->fy, &S->fz};
     for (auto* p : d)
@@ -669,8 +671,8 @@ dsea_status ensure_aos(dsea_ctx* c, size_t doubles)
 
 // Bin the flat host state (by id) into the slots of the input buffer.  The atoms are
 // grouped on the host by destination slice (the same IEEE floor(x / l_x) as the
-// device, Q4) into runs of slices whose atoms fit the staging buffer (a pool of
-// stg_pool slices on a ring), and each group is uploaded and binned on its own; the
+// device, Q4) into runs of at most inb.perm_slots slices whose atoms fit the staging
+// buffer (a pool of stg_pool slices on a ring), and each group is uploaded and binned on its own; the
 // slot contents do not depend on the grouping (cells are ordered by (z, id), Q21).
 dsea_status upload_state(dsea_ctx* c, const double* xyz, const double* v, const double* f)
 {
@@ -694,10 +696,12 @@ dsea_status upload_state(dsea_ctx* c, const double* xyz, const double* v, const 
         for (int64_t i = 0; i < N; i++) order[(size_t)cur[(size_t)slice_of[(size_t)i]]++] = (int32_t)i;
     }
     std::vector<int32_t>().swap(slice_of);
+    // a group binds at most perm_slots slices (the bin scratch holds one slot per slice)
+    const int maxs = std::max(1, c->inb.perm_slots);
     size_t max_group = 0;
     for (int m0 = 0; m0 < ns;) {   // largest group that fits the staging buffer
         int m1 = m0 + 1;
-        while (m1 < ns && (size_t)(count[(size_t)m1 + 1] - count[(size_t)m0]) <= stg_cap) m1++;
+        while (m1 < ns && m1 - m0 < maxs && (size_t)(count[(size_t)m1 + 1] - count[(size_t)m0]) <= stg_cap) m1++;
         const size_t na = (size_t)(count[(size_t)m1] - count[(size_t)m0]);
         if (na > stg_cap)
             return fail(c, DSEA_ECAPACITY, "slice %d holds %zu atoms (staging capacity %zu)", m0, na, stg_cap);
@@ -709,7 +713,7 @@ dsea_status upload_state(dsea_ctx* c, const double* xyz, const double* v, const 
     std::vector<double> hx, hv, hf;
     for (int m0 = 0; m0 < ns;) {
         int m1 = m0 + 1;
-        while (m1 < ns && (size_t)(count[(size_t)m1 + 1] - count[(size_t)m0]) <= stg_cap) m1++;
+        while (m1 < ns && m1 - m0 < maxs && (size_t)(count[(size_t)m1 + 1] - count[(size_t)m0]) <= stg_cap) m1++;
         const int64_t a0 = count[(size_t)m0], na = count[(size_t)m1] - a0;
         if (na > 0) {
             hx.resize((size_t)na * 3); hv.resize((size_t)na * 3); hf.resize((size_t)na * 3);
@@ -837,12 +841,19 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
     NcclApi& api = nccl();
     const int W = c->W;
     auto in_of = [&](int w) -> BufView& { return w == 0 ? c->inb : c->outb[w - 1]; };
+    // pools: slice j of super-cycle K in slot (j + soff) % slots, soff = (K ns) % slots
+    // (BufView.soff); views of a buffer / staging buffer for the ops of cycle K
+    auto soff_of = [&](int cycle, int slots) {
+        return (int)(((int64_t)(cycle % slots) * (int64_t)(ns % slots)) % slots);
+    };
+    auto buf_at = [&](const BufView& B, int cycle) { BufView v = B; v.soff = soff_of(cycle, B.nslots); return v; };
+    auto stg_at = [&](int w, int cycle) { StgView v = c->stg[w]; v.soff = soff_of(cycle, v.pool); return v; };
     // copy slices [j, j+n) between slot buffers of dst_slots / src_slots slots (slice s in
-    // slot s % slots): one cudaMemcpyAsync per run that wraps around neither buffer
-    auto copy_run = [&](char* dst, int dst_slots, const char* src, int src_slots, int j, int n,
-                        cudaStream_t st) -> dsea_status {
+    // slot (s + off) % slots): one cudaMemcpyAsync per run that wraps around neither buffer
+    auto copy_run = [&](char* dst, int dst_slots, int dst_off, const char* src, int src_slots, int src_off, int j,
+                        int n, cudaStream_t st) -> dsea_status {
         for (int k = 0; k < n;) {
-            const int sd = (j + k) % dst_slots, ss_ = (j + k) % src_slots;
+            const int sd = (j + k + dst_off) % dst_slots, ss_ = (j + k + src_off) % src_slots;
             const int run = std::min(n - k, std::min(dst_slots - sd, src_slots - ss_));
             CUDA_TRY(c, cudaMemcpyAsync(dst + (size_t)sd * sb, src + (size_t)ss_ * sb, sb * run,
                                         cudaMemcpyDeviceToDevice, st));
@@ -852,19 +863,21 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
     };
     // the last worker's output pool: before slices [m, m+n) are written into it, the
     // hops that read the previous occupants of those slots must be done
-    auto wait_pool = [&](int m, int n, cudaStream_t st) -> dsea_status {
+    auto wait_pool = [&](int m, int n, int cycle, cudaStream_t st) -> dsea_status {
         BufView& ob = c->outb[W - 1];
+        const int off = soff_of(cycle, ob.nslots);
         for (int sl = m; sl < m + n; sl++) {
-            const int p = sl % ob.nslots;
+            const int p = (sl + off) % ob.nslots;
             if (p < (int)c->pslot_rec.size() && c->pslot_rec[(size_t)p])
                 CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_pslot[(size_t)p], 0));
         }
         return DSEA_OK;
     };
-    auto record_pool = [&](int m, int n, cudaStream_t st) -> dsea_status {
+    auto record_pool = [&](int m, int n, int cycle, cudaStream_t st) -> dsea_status {
         BufView& ob = c->outb[W - 1];
+        const int off = soff_of(cycle, ob.nslots);
         for (int sl = m; sl < m + n; sl++) {
-            const int p = sl % ob.nslots;
+            const int p = (sl + off) % ob.nslots;
             if (p >= (int)c->pslot_rec.size()) continue;
             CUDA_TRY(c, cudaEventRecord(c->ev_pslot[(size_t)p], st));
             c->pslot_rec[(size_t)p] = 1;
@@ -939,19 +952,19 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             }
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
             c->stats.kernel_launches +=
-                force_launch(c->g, c->T, in_of(w), c->stg[w], c->outb[w].cnt, j, n, c->err_dev, c->cs);
+                force_launch(c->g, c->T, in_of(w), stg_at(w, op.cycle), c->outb[w].cnt, j, n, c->err_dev, c->cs);
             c->stats.force_launches++;
             if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_FORCE, {t0, t1}}); }
             if (c->g.thermo) {  // NVT: lambda_j on the critical path, then the drift
                 UnitEnergy* eo = c->e_dev + (size_t)op.t_rel * ns;
-                energy_launch(c->g, c->T, c->stg[w], j, n, eo, c->cs);
-                drift_launch(c->g, c->stg[w], j, n, eo, c->outb[w].cnt, c->err_dev, c->cs);
+                energy_launch(c->g, c->T, stg_at(w, op.cycle), j, n, eo, c->cs);
+                drift_launch(c->g, stg_at(w, op.cycle), j, n, eo, c->outb[w].cnt, c->err_dev, c->cs);
                 CUDA_TRY(c, cudaEventRecord(ev_e, c->cs));
                 c->stats.kernel_launches += 2;
             } else {  // per-slice energy reduction off the critical path
                 CUDA_TRY(c, cudaEventRecord(c->ev_force[w], c->cs));
                 CUDA_TRY(c, cudaStreamWaitEvent(c->es, c->ev_force[w], 0));
-                energy_launch(c->g, c->T, c->stg[w], j, n, c->e_dev + (size_t)op.t_rel * ns, c->es);
+                energy_launch(c->g, c->T, stg_at(w, op.cycle), j, n, c->e_dev + (size_t)op.t_rel * ns, c->es);
                 CUDA_TRY(c, cudaEventRecord(ev_e, c->es));
                 c->stats.kernel_launches++;
             }
@@ -1030,11 +1043,12 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             char* dst_base = to_succ ? c->succ_in_base : c->outb[w].base;
             const int dst_slots = to_succ ? ns : c->outb[w].nslots;
             if (!to_succ && w == W - 1 && c->NG > 1) {
-                dsea_status s = wait_pool(j, n, c->cs);
+                dsea_status s = wait_pool(j, n, op.cycle, c->cs);
                 if (s) return s;
             }
             if (src.base != dst_base) {
-                dsea_status s = copy_run(dst_base, dst_slots, src.base, src.nslots, j, n, c->cs);
+                dsea_status s = copy_run(dst_base, dst_slots, soff_of(op.cycle, dst_slots), src.base, src.nslots,
+                                         soff_of(op.cycle, src.nslots), j, n, c->cs);
                 if (s) return s;
             }
             if (w == 0 && c->NG > 1) {
@@ -1060,16 +1074,17 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 // the successor's arrival flags -- neither needs an SM, so both overlap
                 // the next block's (persistent, SM-filling) force pass
                 {   // the pushes that read the previous occupants of these pool slots
-                    dsea_status s = wait_pool(m, n, c->cs);
+                    dsea_status s = wait_pool(m, n, op.cycle, c->cs);
                     if (s) return s;
                 }
                 cudaEvent_t t0 = nullptr, t1 = nullptr;
                 if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
                 const int s0 = std::max(m - 1, 0), s1 = std::min(m + n, ns - 1);
-                BufView& ob = c->outb[w];
+                const BufView ob = buf_at(c->outb[w], op.cycle);
+                const StgView sv = stg_at(w, op.cycle);
                 bin_scan_launch(c->g, ob, m, n, c->err_dev, c->cs);
-                bin_place_launch(c->g, ob, c->stg[w], s0, s1 - s0 + 1, 0, m, n, c->err_dev, c->cs);
-                bin_gather_launch(c->g, ob, c->stg[w], m, n, c->err_dev, c->cs);
+                bin_place_launch(c->g, ob, sv, s0, s1 - s0 + 1, 0, m, n, c->err_dev, c->cs);
+                bin_gather_launch(c->g, ob, sv, m, n, c->err_dev, c->cs);
                 c->stats.kernel_launches += 3;
                 if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_BIN, {t0, t1}}); }
                 const uint32_t wv = ++c->wr_cnt[m];
@@ -1089,7 +1104,7 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 cudaEvent_t h0 = nullptr, h1 = nullptr;
                 if (c->timing) { h0 = tev(c); h1 = tev(c); cudaEventRecord(h0, c->bs); }
                 {
-                    dsea_status s = copy_run(c->succ_in_base, ns, ob.base, ob.nslots, m, n, c->bs);
+                    dsea_status s = copy_run(c->succ_in_base, ns, 0, ob.base, ob.nslots, ob.soff, m, n, c->bs);
                     if (s) return s;
                 }
                 if (c->ctr) {
@@ -1103,7 +1118,7 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 }
                 if (c->timing) { cudaEventRecord(h1, c->bs); c->tpairs.push_back({TK_SEND, {h0, h1}}); }
                 {
-                    dsea_status s = record_pool(m, n, c->bs);
+                    dsea_status s = record_pool(m, n, op.cycle, c->bs);
                     if (s) return s;
                 }
                 c->stats.hop_bytes += (int64_t)sb * n;
@@ -1128,17 +1143,18 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 } else {
                     for (int sl = m; sl < m + n; sl++)
                         if (sent[sl]) CUDA_TRY(c, cudaStreamWaitEvent(c->cs, c->ev_send[sl], 0));
-                    dsea_status s = wait_pool(m, n, c->cs);
+                    dsea_status s = wait_pool(m, n, op.cycle, c->cs);
                     if (s) return s;
                 }
             }
             cudaEvent_t t0 = nullptr, t1 = nullptr;
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, bst); }
             const int s0 = std::max(m - 1, 0), s1 = std::min(m + n, ns - 1);
-            BufView& ob = c->outb[w];
+            const BufView ob = buf_at(c->outb[w], op.cycle);
+            const StgView sv = stg_at(w, op.cycle);
             bin_scan_launch(c->g, ob, m, n, c->err_dev, bst);
-            bin_place_launch(c->g, ob, c->stg[w], s0, s1 - s0 + 1, 0, m, n, c->err_dev, bst);
-            bin_gather_launch(c->g, ob, c->stg[w], m, n, c->err_dev, bst);
+            bin_place_launch(c->g, ob, sv, s0, s1 - s0 + 1, 0, m, n, c->err_dev, bst);
+            bin_gather_launch(c->g, ob, sv, m, n, c->err_dev, bst);
             c->stats.kernel_launches += 3;
             if (c->timing) { cudaEventRecord(t1, bst); c->tpairs.push_back({TK_BIN, {t0, t1}}); }
             if (w == W - 1 && c->NG > 1) {
@@ -1167,7 +1183,8 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             api.GroupStart();
             for (size_t q = oi; q < oe; q++) {
                 const BufView& ob = c->outb[W - 1];
-                ncclResult_t r = api.Send(ob.base + (size_t)(ops[q].slice % ob.nslots) * sb, sb, ncclChar, 1,
+                const int slot = (ops[q].slice + soff_of(ops[q].cycle, ob.nslots)) % ob.nslots;
+                ncclResult_t r = api.Send(ob.base + (size_t)slot * sb, sb, ncclChar, 1,
                                           c->send_comm, c->ss);
                 if (r != ncclSuccess) { api.GroupEnd(); return fail(c, DSEA_EPEER, "ncclSend: %s", api.GetErrorString(r)); }
             }
@@ -1178,7 +1195,7 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 CUDA_TRY(c, cudaEventRecord(c->ev_send[ops[q].slice], c->ss));
                 sent[ops[q].slice] = 1;
                 c->stats.hop_bytes += (int64_t)sb;
-                dsea_status s = record_pool(ops[q].slice, 1, c->ss);
+                dsea_status s = record_pool(ops[q].slice, 1, ops[q].cycle, c->ss);
                 if (s) return s;
             }
             oi = oe - 1;
@@ -1402,9 +1419,12 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
         int bmax = 1;
         for (int k = 0; k < c->bl.n(); k++) bmax = std::max(bmax, c->bl.count(k));
         const bool staged = mode == DSEA_MODE_STAGED;
-        c->stg_pool = (staged && c->T.kind == FORCE_TILE) ? std::min(g.ns, 2 * bmax + 4) : g.ns;
         const char* hop = getenv("DSEA_PEER_HOP");
-        const bool sm_hop = hop && std::strcmp(hop, "sm") == 0;   // remote stores need the full buffer
+        // remote stores need the full buffers: the successor's slots are written directly,
+        // and the remote bins run on their own stream, unordered with the next force pass
+        // that would rewrite a pooled staging slot
+        const bool sm_hop = c->NG > 1 && hop && std::strcmp(hop, "sm") == 0;
+        c->stg_pool = (staged && c->T.kind == FORCE_TILE && !sm_hop) ? std::min(g.ns, 2 * bmax + 4) : g.ns;
         c->out_pool = (c->NG > 1 && !sm_hop) ? std::min(g.ns, 4 * bmax + 4) : g.ns;
         if (const char* e = getenv("DSEA_FULL_POOLS"); e && *e && atoi(e) != 0) c->stg_pool = c->out_pool = g.ns;
     }

@@ -76,15 +76,22 @@ struct BufView {
     int nslots;      // slots of the buffer: slice j lives in slot j % nslots (a pool of
                      // nslots < ns slots when only a window of slices is ever live,
                      // P:121-122 "s slots", s N_b > N_S; NEXT-3)
-    int perm_slots;  // slots of the bin scratch: slice m uses perm[(m % perm_slots) * cap ..]
+    int perm_slots;  // slots of the bin scratch: slice m uses perm[((m + soff) % perm_slots) * cap ..]
+    int soff;        // slot offset of the launch: slice j of super-cycle K lives in slot
+                     // (j + soff) % nslots with soff = (K ns) % nslots, i.e. slots follow the
+                     // global sequence number K ns + j, so a window of live slices that spans
+                     // a super-cycle boundary (the previous cycle's last slice is finalised
+                     // after the next cycle's first block) never aliases; 0 for a full buffer
 };
 
 // Device view of a staging buffer (flat SoA over ns*cap entries).
 struct StgView {
-    // staged atom i of slice j at index (j % pool) * cap + i (a pool of `pool` slices)
+    // staged atom i of slice j at index ((j + soff) % pool) * cap + i (a pool of `pool`
+    // slices; soff as in BufView)
     double *x, *y, *z, *vx, *vy, *vz, *fx, *fy, *fz;
     int32_t *id, *key;
     int pool;        // slices the arrays hold (ns in the fused pass; a window on a ring)
+    int soff;        // slot offset of the launch (BufView.soff)
     int32_t* n;      // [ns] atoms staged per slice
     double4* eatom;  // energy records (u_core, vir2, ke2, pairs) of the last force pass:
                      // FORCE_TILE one per tile [ns*tiles], FORCE_PIPE one per atom [ns*cap]

@@ -99,3 +99,22 @@ def test_full_size_bench_grid_sampled_planes():
         lo, hi = max(a - n, 0), min(b + n, c.nx)
         ref = OG.run(u0[lo:hi], c.r, n)[a - lo:b - lo]
         assert np.array_equal(out[a:b], ref), (a, b)
+
+
+@pytest.mark.parametrize("env", [{"DSEA_FTCS": "col"}, {"DSEA_FTCS_GRID": "3", "DSEA_FTCS_ROWS": "2"},
+                                 {"DSEA_FTCS_NS": "2", "DSEA_FTCS_ROWS": "1", "DSEA_FTCS_GRID": "5"},
+                                 {"DSEA_FTCS_NS": "4", "DSEA_FTCS_ROWS": "3"}])
+@pytest.mark.parametrize("shape,ns", [((48, 12, 10), 12), ((20, 64, 40), 5), ((33, 7, 34), 11)])
+def test_stencil_kernel_variants_bit_exact(monkeypatch, env, shape, ns):
+    """The bulk-copy plane pipeline (k_ftcs_tma) with forced tilings -- one-row y-tiles,
+    several items per CTA (the load sequence running on across items), 2 and 4 stages
+    -- and the register-column kernel (odd nz always takes it): bit-exact vs the
+    oracle on ragged shapes, fused and on the staged plan."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    c = GridConfig("t", *shape, ns, r=0.11, seed=5)
+    u0, out, _ = _run(c, 5)
+    assert np.array_equal(out, OG.run(u0, c.r, 5))
+    W = 2 if ns >= 8 else 1               # the staged plan needs >= 2 + W blocks
+    u0, out, _ = _run(c, 5, workers_per_gpu=W, slices_per_stage=2, mode=DSEA_GRID_MODE_STAGED)
+    assert np.array_equal(out, OG.run(u0, c.r, 5))
