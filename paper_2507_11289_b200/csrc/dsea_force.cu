@@ -52,6 +52,9 @@ constexpr int TILE_LM = DSEA_TILE_LM;           // hit-list rows per home atom (
 #ifndef DSEA_STAGE_SHFL
 #define DSEA_STAGE_SHFL 1
 #endif
+#ifndef DSEA_STAGE_SU
+#define DSEA_STAGE_SU 4  // staged atoms per thread whose loads are in flight together (8: 0.3 % slower)
+#endif
 constexpr int TILE_ROW = 2 * TILE_HOME + DSEA_ROWPAD;   // bytes per hit-list row (+ 4: rows rotate the banks)
 
 // The piece table of one (sub)tile, built by warp 0 one step ahead.
@@ -268,7 +271,7 @@ k_force_tile(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
             // used; warp-wide items (total is even): lanes 2q, 2q+1 hold the atoms of one
             // candidate pair and trade halves so that each writes one 16-byte record
             const double ox = A.ox, oy = A.oy, oz = A.oz;
-            constexpr int SU = 4;
+            constexpr int SU = DSEA_STAGE_SU;
             int col = 0;
             for (int i0 = tid; i0 - lane < total; i0 += SU * TILE_THREADS) {
                 double x[SU], y[SU], z[SU];
