@@ -168,7 +168,8 @@ def run_reference(args, cfg, rank, world):
         oracle.forces_subset(x, g.b, cfg.rc, idx, threads)
     dt = time.perf_counter() - t0
     value = per_step * args.steps / dt
-    sample = (f"per step: Algorithm 1 forces of {per_step} sampled atoms of {n:,} against all {n:,} "
+    sample = (f"forces-only, sampled -- per step: Algorithm 1 forces of {per_step} sampled atoms of {n:,} "
+              f"against all {n:,} "
               f"(all-pairs O(N) each, minimum image y/z) on the {cfg.name} lattice")
     line = {"metric": "atom-timesteps/s", "value": value, "unit": "atom-timesteps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -472,8 +473,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, k, secs = cpu_oracle_rate(cfg, seconds_target=15.0)
         cpu = {"value": rate, "unit": "atom-timesteps/s", "cores": cores, "kind": "oracle",
-               "sample": f"Algorithm 1 forces of {k} sampled atoms of {atoms:,} against all atoms "
-                         f"(O(N^2) oracle, {secs:.1f} s on {cores} threads)"}
+               "sample": f"forces-only, sampled: Algorithm 1 forces of {k} sampled atoms of {atoms:,} "
+                         f"against all atoms (O(N^2) oracle, no kick/drift/binning; {secs:.1f} s on "
+                         f"{cores} threads)"}
 
     if rank == 0:
         line = {

@@ -680,6 +680,32 @@ dsea_status upload_state(dsea_ctx* c, const double* xyz, const double* v, const 
     const int ns = c->g.ns;
     const size_t stg_cap = (size_t)c->stg_pool * c->g.cap;     // flat staging entries
     dsea_status s;
+    if ((size_t)N <= stg_cap && ns <= c->inb.perm_slots) {
+        // everything fits one group (fused pass, full buffers): upload by id as it is,
+        // no host-side grouping (ids = staging index)
+        if ((s = ensure_aos(c, std::max<size_t>((f ? 9 : 6) * (size_t)N, 1)))) return s;
+        double* dx = c->aos_dev;
+        double* dv = c->aos_dev + 3 * (size_t)N;
+        double* df = f ? c->aos_dev + 6 * (size_t)N : nullptr;
+        CUDA_TRY(c, cudaMemcpyAsync(dx, xyz, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, c->cs));
+        CUDA_TRY(c, cudaMemcpyAsync(dv, v, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, c->cs));
+        if (f) CUDA_TRY(c, cudaMemcpyAsync(df, f, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, c->cs));
+        StgView& S = c->stg[0];
+        if (N > 0) {
+            aos_to_stage_launch(S, dx, dv, df, nullptr, (int)N, c->cs);
+            init_keys_launch(c->g, S, (int)N, c->inb.cnt, c->err_dev, c->cs);
+        }
+        bin_scan_launch(c->g, c->inb, 0, ns, c->err_dev, c->cs);
+        if (N > 0) bin_place_launch(c->g, c->inb, S, 0, 0, (int)N, 0, ns, c->err_dev, c->cs);
+        bin_gather_launch(c->g, c->inb, S, 0, ns, c->err_dev, c->cs);
+        c->stats.kernel_launches += N > 0 ? 5 : 2;
+        CUDA_TRY(c, cudaStreamSynchronize(c->cs));
+        CUDA_TRY(c, cudaGetLastError());
+        if ((s = check_dev_err(c))) return s;
+        c->holds_state = true;
+        c->mirror_valid = false;
+        return DSEA_OK;
+    }
     std::vector<int32_t> slice_of((size_t)N);
     std::vector<int64_t> count((size_t)ns + 1, 0);
     for (int64_t i = 0; i < N; i++) {
@@ -1507,6 +1533,26 @@ dsea_status dsea_ring_connect(dsea_ctx* c, const void* ids, int32_t n_ids)
     NcclApi& api = nccl();
     if (!api.ok) return fail(c, DSEA_EPEER, "libnccl.so.2 not loadable");
     CUDA_TRY(c, cudaSetDevice(c->device));
+    // NCCL p2p is a rendezvous: a send of a pooled slot completes only once the
+    // successor posts the receive, which waits on the successor's own progress -- with a
+    // pool, rebinning a slot would wait on that send and the ring can deadlock. The NCCL
+    // (comparison) backend therefore keeps a full-size last output buffer.
+    if (c->out_pool < c->g.ns) {
+        BufView& ob = c->outb[c->W - 1];
+        for (void* q : {(void*)ob.base, (void*)ob.cnt, (void*)ob.perm}) {
+            cudaFree(q);
+            c->dallocs.erase(std::remove(c->dallocs.begin(), c->dallocs.end(), q), c->dallocs.end());
+        }
+        dsea_status s = alloc_buf(c, &ob, c->g.ns, c->g.ns);
+        if (s) return s;
+        for (size_t k = c->ev_pslot.size(); k < (size_t)c->g.ns; k++) {
+            cudaEvent_t e;
+            CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->ev_pslot.push_back(e);
+        }
+        c->pslot_rec.assign((size_t)c->g.ns, 0);
+        c->out_pool = c->g.ns;
+    }
     const ncclUniqueId* u = static_cast<const ncclUniqueId*>(ids);
     const int prev = (c->rank - 1 + c->NG) % c->NG;
     api.GroupStart();
