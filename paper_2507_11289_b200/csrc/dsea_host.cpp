@@ -1452,7 +1452,18 @@ dsea_status dsea_slice(dsea_ctx* c, const dsea_slice_params* sp)
         const bool sm_hop = c->NG > 1 && hop && std::strcmp(hop, "sm") == 0;
         c->stg_pool = (staged && c->T.kind == FORCE_TILE && !sm_hop) ? std::min(g.ns, 2 * bmax + 4) : g.ns;
         c->out_pool = (c->NG > 1 && !sm_hop) ? std::min(g.ns, 4 * bmax + 4) : g.ns;
-        if (const char* e = getenv("DSEA_FULL_POOLS"); e && *e && atoi(e) != 0) c->stg_pool = c->out_pool = g.ns;
+        // pools only where the full buffers would not fit comfortably: full-size staging
+        // and output buffers (no slot arithmetic, no upload grouping) while they take at
+        // most a quarter of the device memory; DSEA_POOLS=1 forces the pools (tests),
+        // DSEA_POOLS=0 forces full buffers (A/B)
+        const size_t full_bytes =
+            (size_t)g.ns * ((size_t)c->W * g.cap * (9 * sizeof(double) + 2 * sizeof(int32_t)) + c->L.slot_bytes +
+                            (size_t)g.cap * sizeof(BinRec));
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        const char* pe = getenv("DSEA_POOLS");
+        const int force = (pe && *pe) ? atoi(pe) : -1;
+        if (force == 0 || (force < 0 && full_bytes * 4 <= total_b)) c->stg_pool = c->out_pool = g.ns;
     }
     // the input buffer is binned into only by the fused pass / a ring of one (all slices
     // at once) and by the upload (groups of <= stg_pool slices)

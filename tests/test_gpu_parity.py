@@ -152,14 +152,18 @@ def test_cutoff_and_slice_thickness_variants(rc, c_per, ns):
     _cells_exact(e, c)
 
 
-@pytest.mark.parametrize("W,B", [(1, 1), (2, 1), (3, 1), (1, 3), (2, 4), (3, 2), (3, 5)])
-def test_ring_of_one_bitwise_equals_fused(W, B):
+@pytest.mark.parametrize("W,B,pools", [(1, 1, 0), (2, 1, 0), (3, 1, 0), (1, 3, 0), (2, 4, 0), (3, 2, 0), (3, 5, 0),
+                                       (1, 1, 1), (1, 3, 1), (2, 4, 1), (3, 5, 1)])
+def test_ring_of_one_bitwise_equals_fused(monkeypatch, W, B, pools):
     """The stage schedule (Table 1 for B = 1; B slices per stage otherwise; W workers
     sequential on one GPU) and the fused whole-domain pass compute the same
     unit results: bitwise equal states after 7 steps (7 is not a multiple of W = 2, 3:
-    pass-through workers, Q15)."""
+    pass-through workers, Q15).  pools = 1: staging buffers of 2 B + 4 slices (slots
+    (K N_S + j) mod pool; the previous super-cycle's last slice is binned after the
+    next one's first block)."""
     ref, c = _engine("P8")
     ref.step(7)
+    monkeypatch.setenv("DSEA_POOLS", "1" if pools else "")
     e, _ = _engine("P8", workers_per_gpu=W, mode=D.DSEA_MODE_STAGED, slices_per_stage=B)
     e.step(7)
     assert np.array_equal(e.positions(), ref.positions())

@@ -89,6 +89,26 @@ def test_ring_bitwise_equals_single_gpu(tmp_path, n, cfg, steps, workers, calls,
     assert int(r["stats"][0]) > 0  # slices really crossed NVLink
 
 
+# slot pools forced (DSEA_POOLS=1; by default they are used only when full buffers would
+# take more than a quarter of the device memory, e.g. the 1e9-atom ring): staging and the
+# last worker's output buffer hold a window of slices in slots (K N_S + j) mod pool
+POOL_CASES = [(2, "P8", 16, 1, 1, 1, "peer"), (2, "P8", 10, 2, 2, 3, "peer"), (4, "P8", 16, 1, 2, 1, "peer"),
+              (4, "P8", 10, 1, 1, 2, "peer"), (2, "P8", 10, 2, 2, 3, "nccl"), (2, "C3", 4, 1, 1, 0, "peer"),
+              (4, "C3", 8, 1, 1, 0, "peer")]
+
+
+@pytest.mark.parametrize("n,cfg,steps,workers,calls,block,hop", POOL_CASES)
+def test_ring_with_slot_pools_bitwise_equals_single_gpu(tmp_path, n, cfg, steps, workers, calls, block, hop):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    x, v, f, s1, e1, _ = _single(cfg, steps)
+    r = _ring(tmp_path, n, cfg, steps, workers, calls, block, hop, env={"DSEA_POOLS": "1"})
+    assert np.array_equal(r["x"], x)
+    assert np.array_equal(r["v"], v)
+    assert np.array_equal(r["f"], f)
+    assert np.array_equal(r["en"], e1)
+
+
 @pytest.mark.parametrize("n,workers,block,hop", [(2, 1, 0, "peer"), (2, 2, 1, "nccl"), (4, 1, 0, "peer")])
 def test_ring_thermostat_bitwise_equals_single_gpu(tmp_path, n, workers, block, hop):
     """NVT (per-slice isokinetic scaling, Q23) needs no exchange beyond the

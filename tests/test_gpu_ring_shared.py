@@ -35,28 +35,31 @@ def _single(cfg, steps):
     return r
 
 
-def _ring(tmp_path, n, cfg, steps, workers, calls, block):
-    out = str(tmp_path / f"shared_{n}_{cfg}_{steps}_{workers}_{calls}_{block}.npz")
+def _ring(tmp_path, n, cfg, steps, workers, calls, block, pools=False):
+    out = str(tmp_path / f"shared_{n}_{cfg}_{steps}_{workers}_{calls}_{block}_{int(pools)}.npz")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={29600 + 11 * n + steps + 3 * workers + block}",
            os.path.join(ROOT, "tests", "ring_worker.py"), "--config", cfg, "--steps", str(steps),
            "--workers", str(workers), "--calls", str(calls), "--block", str(block), "--hop", "peer",
            "--shared-device", "--out", out]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = {**os.environ, "DSEA_POOLS": "1"} if pools else None
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return np.load(out)
 
 
-# (ranks, config, steps, workers per rank, calls, slices per stage (0 = auto))
-CASES = [(2, "P8", 12, 1, 2, 1), (2, "P8", 12, 2, 1, 0), (3, "P8", 13, 1, 1, 0), (3, "P8", 12, 2, 2, 2),
-         (2, "C1", 10, 1, 1, 0), (3, "C1", 9, 2, 2, 1)]
+# (ranks, config, steps, workers per rank, calls, slices per stage (0 = auto), slot pools
+# forced (DSEA_POOLS=1: staging and the last output buffer hold a window of slices))
+CASES = [(2, "P8", 12, 1, 2, 1, False), (2, "P8", 12, 2, 1, 0, False), (3, "P8", 13, 1, 1, 0, False),
+         (3, "P8", 12, 2, 2, 2, False), (2, "C1", 10, 1, 1, 0, False), (3, "C1", 9, 2, 2, 1, False),
+         (2, "P8", 12, 1, 2, 1, True), (3, "P8", 12, 2, 2, 2, True), (3, "C1", 9, 2, 2, 1, True)]
 
 
-@pytest.mark.parametrize("n,cfg,steps,workers,calls,block", CASES)
-def test_shared_device_ring_equals_oracle_and_single_gpu(tmp_path, n, cfg, steps, workers, calls, block):
+@pytest.mark.parametrize("n,cfg,steps,workers,calls,block,pools", CASES)
+def test_shared_device_ring_equals_oracle_and_single_gpu(tmp_path, n, cfg, steps, workers, calls, block, pools):
     c = CONFIGS[cfg]
     s = _single(cfg, steps)
-    r = _ring(tmp_path, n, cfg, steps, workers, calls, block)
+    r = _ring(tmp_path, n, cfg, steps, workers, calls, block, pools)
     g = oracle.geometry(c.nx, c.ny, c.nz, c.rho, c.rc, c.n_slices, c.cells_per_slice_x)
     xo, vo, Fo, eo = oracle.run(s["x0"], s["v0"], np.zeros_like(s["x0"]), g.b, c.rc, c.dt, steps)
     # against the oracle
