@@ -29,17 +29,24 @@ __device__ __forceinline__ void set_err(DevErr* e, int code, int slice, int atom
     }
 }
 
+// slot of sequence number k in a buffer of n slots: k mod n, without a division in the
+// common cases (a full buffer: k < n; one wrap: k < 2n)
+__device__ __forceinline__ int wrap_slot(int k, int n) {
+    if (k >= n) { k -= n; if (k >= n) k %= n; }
+    return k;
+}
+
 __device__ __forceinline__ const int32_t* slot_cs(const BufView& B, int j) {
-    return reinterpret_cast<const int32_t*>(B.base + (size_t)((j + B.soff) % B.nslots) * B.L.slot_bytes);
+    return reinterpret_cast<const int32_t*>(B.base + (size_t)wrap_slot(j + B.soff, B.nslots) * B.L.slot_bytes);
 }
 __device__ __forceinline__ int32_t* slot_cs_w(const BufView& B, int j) {
-    return reinterpret_cast<int32_t*>(B.base + (size_t)((j + B.soff) % B.nslots) * B.L.slot_bytes);
+    return reinterpret_cast<int32_t*>(B.base + (size_t)wrap_slot(j + B.soff, B.nslots) * B.L.slot_bytes);
 }
 __device__ __forceinline__ double* slot_d(const BufView& B, int j, size_t off) {
-    return reinterpret_cast<double*>(B.base + (size_t)((j + B.soff) % B.nslots) * B.L.slot_bytes + off);
+    return reinterpret_cast<double*>(B.base + (size_t)wrap_slot(j + B.soff, B.nslots) * B.L.slot_bytes + off);
 }
 __device__ __forceinline__ int32_t* slot_i(const BufView& B, int j, size_t off) {
-    return reinterpret_cast<int32_t*>(B.base + (size_t)((j + B.soff) % B.nslots) * B.L.slot_bytes + off);
+    return reinterpret_cast<int32_t*>(B.base + (size_t)wrap_slot(j + B.soff, B.nslots) * B.L.slot_bytes + off);
 }
 
 // 1/x in FP64: MUFU approximation + Newton steps.  One step (default) leaves a relative
@@ -73,7 +80,7 @@ __device__ __forceinline__ int cell_coord(double r, double l, int n) {
 
 // staging index of atom i of slice j (StgView.pool, StgView.soff)
 __device__ __forceinline__ size_t stg_index(const StgView& S, int j, int cap, int i) {
-    return (size_t)((j + S.soff) % S.pool) * cap + i;
+    return (size_t)wrap_slot(j + S.soff, S.pool) * cap + i;
 }
 
 // Position update of md_v3b for one atom whose kick is done:

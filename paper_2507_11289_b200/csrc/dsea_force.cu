@@ -222,8 +222,12 @@ __device__ void build_table(const Geo& g, const Tiling& T, const BufView& in, co
 #define DSEA_ABL 0     // ablation builds for timing studies only (1: no pair work, 2: no FP64 pass)
 #endif
 
+#ifndef DSEA_TILE_MINB
+#define DSEA_TILE_MINB (16 / TILE_WARPS)   // resident CTAs per SM the registers must allow
+#endif
+
 template <bool NVT>
-__global__ void __launch_bounds__(TILE_THREADS, 16 / TILE_WARPS)
+__global__ void __launch_bounds__(TILE_THREADS, DSEA_TILE_MINB)
 k_force_tile(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out_cnt, int j0, int nj,
              DevErr* __restrict__ err, unsigned long long* __restrict__ tile_ctr, unsigned long long ctr_base)
 {

@@ -650,7 +650,7 @@ k_bin_place(Geo g, BufView out, StgView stg, int s0, int flat_count, int m0, int
     pdl_release();
     int base, n;
     if (flat_count > 0) { base = 0; n = flat_count; }
-    else { const int s = s0 + blockIdx.y; base = ((s + stg.soff) % stg.pool) * g.cap; n = stg.n[s]; }
+    else { const int s = s0 + blockIdx.y; base = wrap_slot(s + stg.soff, stg.pool) * g.cap; n = stg.n[s]; }
     const int p = blockIdx.x * PLACE_THREADS + threadIdx.x;
     if (p >= n) return;
     const int key = stg.key[base + p];
@@ -666,7 +666,7 @@ k_bin_place(Geo g, BufView out, StgView stg, int s0, int flat_count, int m0, int
         r.z = stg.z[base + p];
         r.src = base + p;
         r.id = stg.id[base + p];
-        out.perm[(size_t)((m + out.soff) % out.perm_slots) * g.cap + pos] = r;
+        out.perm[(size_t)wrap_slot(m + out.soff, out.perm_slots) * g.cap + pos] = r;
     }
 }
 
@@ -700,7 +700,7 @@ k_bin_gather(Geo g, BufView out, StgView stg, int m0)
     if (sub == 0) out.cnt[(size_t)m * g.ncell + c] = 0;
     if (cs[g.ncell] > g.cap) return;  // capacity error already flagged by the scan
     const int n = en - st;
-    const BinRec* R = out.perm + (size_t)((m + out.soff) % out.perm_slots) * g.cap + st;
+    const BinRec* R = out.perm + (size_t)wrap_slot(m + out.soff, out.perm_slots) * g.cap + st;
     double* ox = slot_d(out, m, out.L.off_x);
     double* oy = slot_d(out, m, out.L.off_y);
     double* oz = slot_d(out, m, out.L.off_z);
