@@ -11,6 +11,8 @@ import sys
 import numpy as np
 import pytest
 
+from tests.conftest import run_group
+
 from oracle import grid as OG
 from paper_2507_11289_b200 import GRID_CONFIGS, GridConfig
 from paper_2507_11289_b200.grid import DSEA_GRID_MODE_STAGED, Grid
@@ -71,7 +73,7 @@ def _ring(tmp_path, n, cfg, steps, workers=1, calls=1, block=0):
            "--master-addr=127.0.0.1", f"--master-port={29700 + n * 11 + steps}",
            os.path.join(ROOT, "tests", "grid_ring_worker.py"), "--config", cfg, "--steps", str(steps),
            "--workers", str(workers), "--calls", str(calls), "--block", str(block), "--out", out]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = run_group(cmd, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return np.load(out)
 

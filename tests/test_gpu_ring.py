@@ -11,6 +11,8 @@ import sys
 import numpy as np
 import pytest
 
+from tests.conftest import run_group
+
 from paper_2507_11289_b200 import CONFIGS
 from paper_2507_11289_b200 import dsea as D
 
@@ -49,8 +51,7 @@ def _ring(tmp_path, n, cfg, steps, workers=1, calls=1, block=0, hop="peer", ther
            os.path.join(ROOT, "tests", "ring_worker.py"), "--config", cfg, "--steps", str(steps),
            "--workers", str(workers), "--calls", str(calls), "--block", str(block), "--hop", hop,
            "--thermo", str(thermo), "--out", out]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
-                       env=None if env is None else {**os.environ, **env})
+    r = run_group(cmd, timeout=300, cwd=ROOT, env=None if env is None else {**os.environ, **env})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return np.load(out)
 
@@ -106,6 +107,21 @@ def test_ring_with_slot_pools_bitwise_equals_single_gpu(tmp_path, n, cfg, steps,
     assert np.array_equal(r["x"], x)
     assert np.array_equal(r["v"], v)
     assert np.array_equal(r["f"], f)
+    assert np.array_equal(r["en"], e1)
+
+
+@pytest.mark.parametrize("n,cfg,steps,workers,calls,block,lead", [(4, "P8", 12, 2, 1, 3, False),
+                                                                  (4, "P8", 12, 1, 1, 5, True)])
+def test_nccl_plateau_without_pdl(tmp_path, n, cfg, steps, workers, calls, block, lead):
+    """The two NCCL plateau cases that hang with programmatic dependent launch, run with
+    plain launches (DSEA_PDL=0): diagnoses whether early-resident CTAs starve NCCL's
+    kernels of SMs."""
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    x, v, f, s1, e1, _ = _single(cfg, steps)
+    env = {"DSEA_PDL": "0", **({"DSEA_LEAD_BLOCKS": "1"} if lead else {})}
+    r = _ring(tmp_path, n, cfg, steps, workers, calls, block, "nccl", env=env)
+    assert np.array_equal(r["x"], x)
     assert np.array_equal(r["en"], e1)
 
 

@@ -16,6 +16,8 @@ import sys
 import numpy as np
 import pytest
 
+from tests.conftest import run_group
+
 import oracle
 from paper_2507_11289_b200 import CONFIGS
 from paper_2507_11289_b200 import dsea as D
@@ -43,7 +45,7 @@ def _ring(tmp_path, n, cfg, steps, workers, calls, block, pools=False):
            "--workers", str(workers), "--calls", str(calls), "--block", str(block), "--hop", "peer",
            "--shared-device", "--out", out]
     env = {**os.environ, "DSEA_POOLS": "1"} if pools else None
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    r = run_group(cmd, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return np.load(out)
 
