@@ -29,11 +29,11 @@ __device__ __forceinline__ void set_err(DevErr* e, int code, int slice, int atom
     }
 }
 
-// slot of sequence number k in a buffer of n slots: k mod n, without a division in the
-// common cases (a full buffer: k < n; one wrap: k < 2n)
+// slot of a launch-normalised sequence number k in [-n, 2n) of a buffer of n slots
+// (BufView.soff): one compare, no division -- a division path here doubled the bin
+// gather's registers and halved its occupancy
 __device__ __forceinline__ int wrap_slot(int k, int n) {
-    if (k >= n) { k -= n; if (k >= n) k %= n; }
-    return k;
+    return k >= n ? k - n : (k < 0 ? k + n : k);
 }
 
 __device__ __forceinline__ const int32_t* slot_cs(const BufView& B, int j) {

@@ -562,8 +562,9 @@ Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
         const double per_col = std::min(mean_col + 2.0 * mean_per_cell, home + (2.0 * g.rc + g.l[2]) * dens);
         return 9.0 * per_col + 18.0;
     };
-    // as many resident CTAs per SM as the staging of a full tile allows (4 at rho 0.8,
-    // rc 2.5); denser or longer-ranged workloads get fewer, larger CTAs
+    // as many resident CTAs per SM as the staging of a full tile allows (16 / TILE_WARPS:
+    // 2 CTAs of 8 warps at rho 0.8, rc 2.5); denser or longer-ranged workloads get fewer,
+    // larger CTAs
     int per_sm_smem = 233472;
     int dev = 0;
     cudaGetDevice(&dev);

@@ -604,6 +604,7 @@ dsea_status alloc_buf(dsea_ctx* c, BufView* B, int nslots, int perm_slots)
     B->nslots = nslots;
     B->perm_slots = perm_slots;
     B->soff = 0;
+    B->poff = 0;
     if ((s = dalloc(c, &B->base, c->L.slot_bytes * (size_t)nslots))) return s;
     if ((s = dalloc(c, &B->cnt, (size_t)c->g.ns * c->g.ncell))) return s;
     if ((s = dalloc(c, &B->perm, (size_t)perm_slots * c->g.cap))) return s;
@@ -763,9 +764,11 @@ dsea_status upload_state(dsea_ctx* c, const double* xyz, const double* v, const 
             aos_to_stage_launch(S, dx, dv, df, c->ids_dev, (int)na, c->cs);
             init_keys_launch(c->g, S, (int)na, c->inb.cnt, c->err_dev, c->cs);
         }
-        bin_scan_launch(c->g, c->inb, m0, m1 - m0, c->err_dev, c->cs);
-        if (na > 0) bin_place_launch(c->g, c->inb, c->stg[0], 0, 0, (int)na, m0, m1 - m0, c->err_dev, c->cs);
-        bin_gather_launch(c->g, c->inb, c->stg[0], m0, m1 - m0, c->err_dev, c->cs);
+        BufView ib = c->inb;
+        ib.poff = -m0;                  // the group's slices in bin-scratch slots 0 .. m1-m0-1
+        bin_scan_launch(c->g, ib, m0, m1 - m0, c->err_dev, c->cs);
+        if (na > 0) bin_place_launch(c->g, ib, c->stg[0], 0, 0, (int)na, m0, m1 - m0, c->err_dev, c->cs);
+        bin_gather_launch(c->g, ib, c->stg[0], m0, m1 - m0, c->err_dev, c->cs);
         c->stats.kernel_launches += na > 0 ? 5 : 2;
         CUDA_TRY(c, cudaStreamSynchronize(c->cs));   // the host group buffers are reused
         CUDA_TRY(c, cudaGetLastError());
@@ -872,14 +875,25 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
     auto soff_of = [&](int cycle, int slots) {
         return (int)(((int64_t)(cycle % slots) * (int64_t)(ns % slots)) % slots);
     };
-    auto buf_at = [&](const BufView& B, int cycle) { BufView v = B; v.soff = soff_of(cycle, B.nslots); return v; };
-    auto stg_at = [&](int w, int cycle) { StgView v = c->stg[w]; v.soff = soff_of(cycle, v.pool); return v; };
+    // device views for a launch whose lowest slice is jmin: offsets normalised so that
+    // j + off lies in [0, 2 slots) for the launch's slices (BufView.soff)
+    auto norm = [&](int cycle, int slots, int jmin) {
+        return (int)(((int64_t)jmin + soff_of(cycle, slots)) % slots) - jmin;
+    };
+    auto buf_at = [&](const BufView& B, int cycle, int jmin) {
+        BufView v = B;
+        v.soff = norm(cycle, B.nslots, jmin);
+        v.poff = norm(cycle, B.perm_slots, jmin);
+        return v;
+    };
+    auto stg_at = [&](int w, int cycle, int jmin) { StgView v = c->stg[w]; v.soff = norm(cycle, v.pool, jmin); return v; };
     // copy slices [j, j+n) between slot buffers of dst_slots / src_slots slots (slice s in
     // slot (s + off) % slots): one cudaMemcpyAsync per run that wraps around neither buffer
     auto copy_run = [&](char* dst, int dst_slots, int dst_off, const char* src, int src_slots, int src_off, int j,
                         int n, cudaStream_t st) -> dsea_status {
         for (int k = 0; k < n;) {
-            const int sd = (j + k + dst_off) % dst_slots, ss_ = (j + k + src_off) % src_slots;
+            const int sd = (int)((((int64_t)j + k + dst_off) % dst_slots + dst_slots) % dst_slots);
+            const int ss_ = (int)((((int64_t)j + k + src_off) % src_slots + src_slots) % src_slots);
             const int run = std::min(n - k, std::min(dst_slots - sd, src_slots - ss_));
             CUDA_TRY(c, cudaMemcpyAsync(dst + (size_t)sd * sb, src + (size_t)ss_ * sb, sb * run,
                                         cudaMemcpyDeviceToDevice, st));
@@ -978,19 +992,19 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             }
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
             c->stats.kernel_launches +=
-                force_launch(c->g, c->T, in_of(w), stg_at(w, op.cycle), c->outb[w].cnt, j, n, c->err_dev, c->cs);
+                force_launch(c->g, c->T, in_of(w), stg_at(w, op.cycle, j), c->outb[w].cnt, j, n, c->err_dev, c->cs);
             c->stats.force_launches++;
             if (c->timing) { cudaEventRecord(t1, c->cs); c->tpairs.push_back({TK_FORCE, {t0, t1}}); }
             if (c->g.thermo) {  // NVT: lambda_j on the critical path, then the drift
                 UnitEnergy* eo = c->e_dev + (size_t)op.t_rel * ns;
-                energy_launch(c->g, c->T, stg_at(w, op.cycle), j, n, eo, c->cs);
-                drift_launch(c->g, stg_at(w, op.cycle), j, n, eo, c->outb[w].cnt, c->err_dev, c->cs);
+                energy_launch(c->g, c->T, stg_at(w, op.cycle, j), j, n, eo, c->cs);
+                drift_launch(c->g, stg_at(w, op.cycle, j), j, n, eo, c->outb[w].cnt, c->err_dev, c->cs);
                 CUDA_TRY(c, cudaEventRecord(ev_e, c->cs));
                 c->stats.kernel_launches += 2;
             } else {  // per-slice energy reduction off the critical path
                 CUDA_TRY(c, cudaEventRecord(c->ev_force[w], c->cs));
                 CUDA_TRY(c, cudaStreamWaitEvent(c->es, c->ev_force[w], 0));
-                energy_launch(c->g, c->T, stg_at(w, op.cycle), j, n, c->e_dev + (size_t)op.t_rel * ns, c->es);
+                energy_launch(c->g, c->T, stg_at(w, op.cycle, j), j, n, c->e_dev + (size_t)op.t_rel * ns, c->es);
                 CUDA_TRY(c, cudaEventRecord(ev_e, c->es));
                 c->stats.kernel_launches++;
             }
@@ -1106,8 +1120,8 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
                 cudaEvent_t t0 = nullptr, t1 = nullptr;
                 if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, c->cs); }
                 const int s0 = std::max(m - 1, 0), s1 = std::min(m + n, ns - 1);
-                const BufView ob = buf_at(c->outb[w], op.cycle);
-                const StgView sv = stg_at(w, op.cycle);
+                const BufView ob = buf_at(c->outb[w], op.cycle, s0);
+                const StgView sv = stg_at(w, op.cycle, s0);
                 bin_scan_launch(c->g, ob, m, n, c->err_dev, c->cs);
                 bin_place_launch(c->g, ob, sv, s0, s1 - s0 + 1, 0, m, n, c->err_dev, c->cs);
                 bin_gather_launch(c->g, ob, sv, m, n, c->err_dev, c->cs);
@@ -1176,8 +1190,8 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
             cudaEvent_t t0 = nullptr, t1 = nullptr;
             if (c->timing) { t0 = tev(c); t1 = tev(c); cudaEventRecord(t0, bst); }
             const int s0 = std::max(m - 1, 0), s1 = std::min(m + n, ns - 1);
-            const BufView ob = buf_at(c->outb[w], op.cycle);
-            const StgView sv = stg_at(w, op.cycle);
+            const BufView ob = buf_at(c->outb[w], op.cycle, s0);
+            const StgView sv = stg_at(w, op.cycle, s0);
             bin_scan_launch(c->g, ob, m, n, c->err_dev, bst);
             bin_place_launch(c->g, ob, sv, s0, s1 - s0 + 1, 0, m, n, c->err_dev, bst);
             bin_gather_launch(c->g, ob, sv, m, n, c->err_dev, bst);

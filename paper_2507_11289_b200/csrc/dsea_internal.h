@@ -76,12 +76,15 @@ struct BufView {
     int nslots;      // slots of the buffer: slice j lives in slot j % nslots (a pool of
                      // nslots < ns slots when only a window of slices is ever live,
                      // P:121-122 "s slots", s N_b > N_S; NEXT-3)
-    int perm_slots;  // slots of the bin scratch: slice m uses perm[((m + soff) % perm_slots) * cap ..]
+    int perm_slots;  // slots of the bin scratch: slice m uses perm[wrap(m + poff, perm_slots) * cap ..]
     int soff;        // slot offset of the launch: slice j of super-cycle K lives in slot
-                     // (j + soff) % nslots with soff = (K ns) % nslots, i.e. slots follow the
-                     // global sequence number K ns + j, so a window of live slices that spans
-                     // a super-cycle boundary (the previous cycle's last slice is finalised
-                     // after the next cycle's first block) never aliases; 0 for a full buffer
+                     // (K ns + j) mod nslots -- slots follow the global sequence number, so a
+                     // window of live slices that spans a super-cycle boundary (the previous
+                     // cycle's last slice is finalised after the next cycle's first block)
+                     // never aliases.  The host normalises soff to the launch's lowest slice,
+                     // so j + soff lies in [0, 2 nslots) and the kernels wrap with one compare
+                     // (wrap_slot); 0 for a full buffer
+    int poff;        // the same for the bin scratch (perm_slots)
 };
 
 // Device view of a staging buffer (flat SoA over ns*cap entries).

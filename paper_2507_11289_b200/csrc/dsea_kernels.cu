@@ -666,7 +666,7 @@ k_bin_place(Geo g, BufView out, StgView stg, int s0, int flat_count, int m0, int
         r.z = stg.z[base + p];
         r.src = base + p;
         r.id = stg.id[base + p];
-        out.perm[(size_t)wrap_slot(m + out.soff, out.perm_slots) * g.cap + pos] = r;
+        out.perm[(size_t)wrap_slot(m + out.poff, out.perm_slots) * g.cap + pos] = r;
     }
 }
 
@@ -681,6 +681,9 @@ k_bin_place(Geo g, BufView out, StgView stg, int s0, int flat_count, int m0, int
 constexpr int GATHER_THREADS = 256;
 constexpr int GATHER_CELLS = GATHER_THREADS / 16;   // cells per CTA
 
+// 32 registers = 8 CTAs of 256 threads per SM: the gather is latency-bound (a cell's
+// records, then its staged atoms) and needs every resident warp.  A division on the
+// slot path (wrap_slot) once took it to 64 registers and half the occupancy (1.8x slower).
 template <int CM>
 __global__ void __launch_bounds__(GATHER_THREADS)
 k_bin_gather(Geo g, BufView out, StgView stg, int m0)
@@ -700,23 +703,22 @@ k_bin_gather(Geo g, BufView out, StgView stg, int m0)
     if (sub == 0) out.cnt[(size_t)m * g.ncell + c] = 0;
     if (cs[g.ncell] > g.cap) return;  // capacity error already flagged by the scan
     const int n = en - st;
-    const BinRec* R = out.perm + (size_t)wrap_slot(m + out.soff, out.perm_slots) * g.cap + st;
-    double* ox = slot_d(out, m, out.L.off_x);
-    double* oy = slot_d(out, m, out.L.off_y);
-    double* oz = slot_d(out, m, out.L.off_z);
-    double* ovx = slot_d(out, m, out.L.off_vx);
-    double* ovy = slot_d(out, m, out.L.off_vy);
-    double* ovz = slot_d(out, m, out.L.off_vz);
-    double* ofx = slot_d(out, m, out.L.off_fx);
-    double* ofy = slot_d(out, m, out.L.off_fy);
-    double* ofz = slot_d(out, m, out.L.off_fz);
-    int32_t* oid = slot_i(out, m, out.L.off_id);
+    const BinRec* R = out.perm + (size_t)wrap_slot(m + out.poff, out.perm_slots) * g.cap + st;
+    // one slot base in a register; the array offsets stay kernel parameters (10 live
+    // 64-bit pointers would double the register count and halve the occupancy)
+    char* const sb = out.base + (size_t)wrap_slot(m + out.soff, out.nslots) * out.L.slot_bytes;
     auto put = [&](int src, double z, int id, int rank) {
-        const int d = st + rank;
-        ox[d] = stg.x[src]; oy[d] = stg.y[src]; oz[d] = z;
-        ovx[d] = stg.vx[src]; ovy[d] = stg.vy[src]; ovz[d] = stg.vz[src];
-        ofx[d] = stg.fx[src]; ofy[d] = stg.fy[src]; ofz[d] = stg.fz[src];
-        oid[d] = id;
+        const size_t d8 = (size_t)(st + rank) * sizeof(double);
+        *reinterpret_cast<double*>(sb + out.L.off_x + d8) = stg.x[src];
+        *reinterpret_cast<double*>(sb + out.L.off_y + d8) = stg.y[src];
+        *reinterpret_cast<double*>(sb + out.L.off_z + d8) = z;
+        *reinterpret_cast<double*>(sb + out.L.off_vx + d8) = stg.vx[src];
+        *reinterpret_cast<double*>(sb + out.L.off_vy + d8) = stg.vy[src];
+        *reinterpret_cast<double*>(sb + out.L.off_vz + d8) = stg.vz[src];
+        *reinterpret_cast<double*>(sb + out.L.off_fx + d8) = stg.fx[src];
+        *reinterpret_cast<double*>(sb + out.L.off_fy + d8) = stg.fy[src];
+        *reinterpret_cast<double*>(sb + out.L.off_fz + d8) = stg.fz[src];
+        *reinterpret_cast<int32_t*>(sb + out.L.off_id + (size_t)(st + rank) * sizeof(int32_t)) = id;
     };
     if (n <= CM) {
         for (int e = sub; e < n; e += 16) {
