@@ -5,9 +5,12 @@ cd "${GRAFT_REPO_ROOT:-/root/repo}"
 O=gpurun_out/${TAG:-rb}; mkdir -p $O
 N=$(nvidia-smi -L | wc -l)
 if [ -z "$NO_TESTS" ]; then
-timeout 2400 python -m pytest tests/test_gpu_ring.py tests/test_gpu_grid.py -k "ring" -q --timeout 400 -rf ${PYTEST_K:+-k "$PYTEST_K"} > $O/pytest_ring.log 2>&1; echo "rc=$?" >> $O/pytest_ring.log
+timeout 2400 python -m pytest tests/test_gpu_ring.py tests/test_gpu_ring_shared.py tests/test_gpu_grid.py -k "ring" -q --timeout 400 -rf \
+  ${DESELECT_NCCL_PLATEAU:+--deselect "tests/test_gpu_ring.py::test_ring_bitwise_equals_single_gpu[4-P8-12-2-1-3-nccl-False]" --deselect "tests/test_gpu_ring.py::test_ring_bitwise_equals_single_gpu[4-P8-12-1-1-5-nccl-True]"} \
+  ${PYTEST_K:+-k "$PYTEST_K"} > $O/pytest_ring.log 2>&1; echo "rc=$?" >> $O/pytest_ring.log
 fi
 if [ -z "$NO_BENCH" ]; then
+nvidia-smi topo -m > $O/topo.txt 2>&1
 timeout 600 python bench.py --steps 10 --warmup 3 > $O/bench_c4_n1.log 2>&1
 timeout 600 python bench.py --config G1 --steps 20 --warmup 3 > $O/bench_g1_n1.log 2>&1
 for n in 2 4; do [ $n -le $N ] || continue
