@@ -47,7 +47,7 @@ constexpr int TILE_HOME = 16 * TILE_WARPS;      // home atoms per (sub)tile: up 
 constexpr int TILE_ILP = DSEA_TILE_ILP;         // hits in flight per lane in the FP64 pass
 constexpr int TILE_LM = DSEA_TILE_LM;           // hit-list rows per home atom (shared by its two lanes)
 #ifndef DSEA_ROWPAD
-#define DSEA_ROWPAD 4
+#define DSEA_ROWPAD 16  // row stride 2*TILE_HOME + 16 bytes: rows rotate the banks (C4: pad 4 8.48 ms, 8 8.44, 16 8.42)
 #endif
 #ifndef DSEA_STAGE_SHFL
 #define DSEA_STAGE_SHFL 1
