@@ -55,7 +55,7 @@ constexpr int TILE_LM = DSEA_TILE_LM;           // hit-list rows per home atom (
 #ifndef DSEA_STAGE_SU
 #define DSEA_STAGE_SU 4  // staged atoms per thread whose loads are in flight together (8: 0.3 % slower)
 #endif
-constexpr int TILE_ROW = 2 * TILE_HOME + DSEA_ROWPAD;   // bytes per hit-list row (+ 4: rows rotate the banks)
+constexpr int TILE_ROW = 2 * TILE_HOME + DSEA_ROWPAD;   // bytes per hit-list row (the pad rotates the banks)
 
 // The piece table of one (sub)tile, built by warp 0 one step ahead.
 struct TileTable {
