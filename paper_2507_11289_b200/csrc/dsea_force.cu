@@ -4,7 +4,7 @@
 // and destination decision of md_v3b for the atoms of slices
 // [j0, j0 + nj), each reading its left and right neighbour slices (O_in = 1).
 //
-// A tile is up to TILE_HOME consecutive, z-sorted home atoms of one (cx, cy) column of
+// A tile is up to TILE_ATOMS consecutive, z-sorted home atoms of one (cx, cy) column of
 // slice j.  Persistent CTAs (a few per SM) claim tiles from a counter; per tile:
 //   1. a piece table: 9 neighbour columns x {low z-image, main run, high z-image}, the
 //      cells within one cell (l >= rc) of the home atoms' cells (periodic images in y
@@ -43,7 +43,12 @@ namespace dsea {
 #endif
 constexpr int TILE_WARPS = DSEA_TILE_WARPS;
 constexpr int TILE_THREADS = 32 * TILE_WARPS;
-constexpr int TILE_HOME = 16 * TILE_WARPS;      // home atoms per (sub)tile: up to one chunk per warp
+constexpr int TILE_HOME = 16 * TILE_WARPS;      // home atoms in flight: one 16-atom chunk per warp
+#ifndef DSEA_TILE_CHUNKS
+#define DSEA_TILE_CHUNKS TILE_WARPS
+#endif
+constexpr int TILE_CHUNKS = DSEA_TILE_CHUNKS;   // 16-atom chunks per tile (claimed by the warps)
+constexpr int TILE_ATOMS = 16 * TILE_CHUNKS;    // home atoms per (sub)tile
 constexpr int TILE_ILP = DSEA_TILE_ILP;         // hits in flight per lane in the FP64 pass
 constexpr int TILE_LM = DSEA_TILE_LM;           // hit-list rows per home atom (shared by its two lanes)
 #ifndef DSEA_ROWPAD
@@ -143,7 +148,7 @@ __device__ void build_table(const Geo& g, const Tiling& T, const BufView& in, co
         return __reduce_add_sync(FULLMASK, n);
     };
     const int czb = cell_of(hb);
-    int he = min(h1, hb + TILE_HOME);
+    int he = min(h1, hb + TILE_ATOMS);
     int cnt = 0, start = 0, src_slice = 0, excl = 0, total = 0, cze = 0;
     double dyv = 0.0, dzv = 0.0;
     bool ok = true;
@@ -235,7 +240,7 @@ k_force_tile(Geo g, Tiling T, BufView in, StgView stg, int32_t* __restrict__ out
     pdl_release();
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ TileTable TT[2];
-    __shared__ double4 s_ce[TILE_WARPS];        // chunk energy records of the current sub-tile
+    __shared__ double4 s_ce[TILE_CHUNKS];       // chunk energy records of the current sub-tile
     __shared__ int s_chunk;                     // next chunk to claim
     __shared__ int s_tbl;                       // the next table has a builder
     // dynamic shared memory (byte offsets from the host: a base ptxas sees as a constant
@@ -550,12 +555,12 @@ Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
     if (kind && std::string(kind) == "pipe") return pipe_tiling(g, mean_per_cell, smem_optin);
     Tiling T{};
     T.kind = FORCE_TILE;
-    T.home = TILE_HOME;
+    T.home = TILE_ATOMS;
     T.maxh = std::max(8, std::min(TILE_LM, (int)env_num("DSEA_MAXH", TILE_LM)));
     const int CZ = g.cells[2];
     const double mean_col = mean_per_cell * CZ;                // atoms per column
     const double dens = mean_per_cell / g.l[2];                 // atoms per sigma of column
-    T.nzt = std::max(1, (int)std::ceil(1.1 * mean_col / TILE_HOME) + 1);
+    T.nzt = std::max(1, (int)std::ceil(1.1 * mean_col / TILE_ATOMS) + 1);
     T.tiles = g.c * g.cells[1] * T.nzt;
     // staged atoms of a full tile: 9 columns x (home extent + 2 rc + a partial cell)
     auto staged = [&](int home) {
@@ -570,7 +575,7 @@ Tiling choose_tiling(const Geo& g, double mean_per_cell, int smem_optin)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     const int stat = tile_static_smem();
-    const int want = ((int)(env_num("DSEA_TILE_MARGIN", 1.1) * staged(TILE_HOME) + 64.0) + 31) / 32 * 32;
+    const int want = ((int)(env_num("DSEA_TILE_MARGIN", 1.1) * staged(TILE_ATOMS) + 64.0) + 31) / 32 * 32;
     const int need16 = ((int)(1.3 * staged(8) + 64.0) + 31) / 32 * 32;    // a small sub-tile
     for (int per_sm = (int)env_num("DSEA_TILE_CTAS", 16 / TILE_WARPS); per_sm >= 1; per_sm--) {
         const long budget = (long)per_sm_smem / per_sm - 1024 - stat;
