@@ -17,8 +17,10 @@ sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(_
 from paper_2507_11289_b200 import dsea as D  # noqa: E402
 
 NS = 109
-T_FORCE_SLICE = 9.85 / NS          # ms, fused C4 force launch / 109 slices
-T_BIN_SLICE = 0.88 / NS            # ms, fused C4 bins / 109 slices
+# round-2 final kernels (profiles/r02/bench_c4_n1.json, launches_bench_n1.csv); round 1:
+# force 9.85 ms, bins 0.88 ms
+T_FORCE_SLICE = 8.40 / NS          # ms, fused C4 force launch / 109 slices
+T_BIN_SLICE = 0.79 / NS            # ms, fused C4 bins / 109 slices
 T_FORCE_LAUNCH = 0.022             # ms per force launch (ramp + tail; timeline)
 T_BIN_LAUNCH = 0.025               # ms per bin run (3 kernels + gaps)
 SLICE_BYTES = 11.4e6
@@ -90,7 +92,8 @@ def simulate(ng, cycles=10, W=1, B=None):
 
 if __name__ == "__main__":
     one = 16_384_000 / ((T_FORCE_SLICE + T_BIN_SLICE) * NS * 1e-3)
-    print(f"model 1 GPU (fused): {one:.3e} atom-timesteps/s (measured 1.523e9)")
+    print(f"model 1 GPU (fused): {one:.3e} atom-timesteps/s (measured 1.776e9; ring4_final: 2 GPUs 90.5 %, "
+          f"4 GPUs 84.9 % of N x one GPU)")
     for ng in [int(a) for a in sys.argv[1:]] or [2, 4, 8]:
         v, ms, B = simulate(ng)
         print(f"model {ng} GPUs, B = {B}: {v:.3e} atom-timesteps/s = {v / (ng * one):.1%} of {ng} x 1 GPU "
