@@ -17,7 +17,7 @@ print("p2p GB/s", 20 * a.numel() / (time.perf_counter() - t) / 1e9)
 PY
 R="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1"
 timeout 600 $R --master-port 29651 bench.py --gpus 2 --steps 10 --warmup 3 --no-cpu-baseline > $O/c4_n2.log 2>&1
-DSEA_FULL_POOLS=1 timeout 600 $R --master-port 29652 bench.py --gpus 2 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/c4_n2_full.log 2>&1
+DSEA_POOLS=0 timeout 600 $R --master-port 29652 bench.py --gpus 2 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/c4_n2_full.log 2>&1
 timeout 600 $R --master-port 29653 bench.py --gpus 2 --config G1 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/g1_n2.log 2>&1
 DSEA_FTCS=col timeout 600 $R --master-port 29654 bench.py --gpus 2 --config G1 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/g1_n2_col.log 2>&1
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > $O/c4_n1.log 2>&1
