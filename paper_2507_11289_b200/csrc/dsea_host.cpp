@@ -18,6 +18,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <array>
 #include <new>
 #include <cmath>
@@ -1760,6 +1762,38 @@ static dsea_status step_chunk(dsea_ctx* c, int64_t n_steps)
     const char* tl_path = c->timing ? getenv("DSEA_TIMELINE") : nullptr;
     if (tl_path) { tl0 = tev(c); cudaEventRecord(tl0, c->cs); }
     dsea_status s = c->mode == DSEA_MODE_FUSED ? run_fused(c, n_steps) : run_plan(c, n_steps);
+    if (const char* hd = getenv("DSEA_HANG_DEBUG"); hd && *hd && c->timing && !s) {
+        // diagnosis of a hung ring: poll the streams; after the given seconds, report per
+        // stream kind how many timed ops completed and which is the first pending one
+        const double limit = atof(hd);
+        const auto t0 = std::chrono::steady_clock::now();
+        cudaStream_t sts[] = {c->cs, c->ss, c->rs, c->es, c->bs};
+        for (;;) {
+            bool idle = true;
+            for (cudaStream_t st : sts) idle = idle && cudaStreamQuery(st) == cudaSuccess;
+            if (idle) break;
+            if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+                const char* names[] = {"force", "bin", "send"};
+                int done[3] = {0, 0, 0}, total[3] = {0, 0, 0}, first[3] = {-1, -1, -1};
+                for (size_t k = 0; k < c->tpairs.size(); k++) {
+                    const int kd = c->tpairs[k].first;
+                    total[kd]++;
+                    if (cudaEventQuery(c->tpairs[k].second.second) == cudaSuccess) done[kd]++;
+                    else if (first[kd] < 0) first[kd] = (int)k;
+                }
+                for (int kd = 0; kd < 3; kd++)
+                    fprintf(stderr, "[dsea hang rank %d] %s: %d of %d done, first pending timed op #%d\n", c->rank,
+                            names[kd], done[kd], total[kd], first[kd]);
+                const char* sn[] = {"compute", "send", "recv", "energy", "hop"};
+                for (int k = 0; k < 5; k++)
+                    fprintf(stderr, "[dsea hang rank %d] stream %s %s\n", c->rank, sn[k],
+                            cudaStreamQuery(sts[k]) == cudaSuccess ? "idle" : "busy");
+                fflush(stderr);
+                break;
+            }
+            std::this_thread::sleep_for(std::chrono::milliseconds(20));
+        }
+    }
     if (s) return s;
     CUDA_TRY(c, cudaStreamSynchronize(c->cs));
     CUDA_TRY(c, cudaStreamSynchronize(c->ss));

@@ -56,6 +56,8 @@ def main():
     e.slice(n_slices=c.n_slices, cells_per_slice_x=c.cells_per_slice_x, n_gpus=world, rank=rank,
             device=local, workers_per_gpu=a.workers, slices_per_stage=a.block)
     _log(rank, "sliced")
+    if os.environ.get("DSEA_HANG_DEBUG"):
+        D.dsea_set_timing(e.ctx, True)     # per-op events for the library's hang report
     if a.thermo > 0:
         e.set_thermostat(a.thermo)
     D.ring_connect(e.ctx, rank, world, a.hop)
