@@ -79,7 +79,7 @@ NCCL_PLATEAU_HANG = {(4, "P8", 12, 2, 1, 3, "nccl", False), (4, "P8", 12, 1, 1, 
 
 
 def _ring_case(c):
-    if c in NCCL_PLATEAU_HANG:
+    if c in NCCL_PLATEAU_HANG and not os.environ.get("DSEA_RUN_XFAIL"):
         return pytest.param(*c, marks=pytest.mark.xfail(run=False, reason="NCCL backend hangs at the 4-GPU "
                                                                              "plateau (DESIGN.md §12)"))
     return c
