@@ -21,7 +21,6 @@
 #include <chrono>
 #include <thread>
 #include <array>
-#include <deque>
 #include <new>
 #include <cmath>
 #include <cstdarg>
@@ -945,41 +944,8 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
     std::vector<Op> ops = P.ops;
     if (c->ctr) order_pushes(ops, W);
     const size_t nops = ops.size();
-    // NCCL backend: enqueue in windows of stages. Enqueuing a whole multi-cycle plan up
-    // front filled NCCL's queue of outstanding operations at Eq. (1)'s plateau, and a
-    // host blocked in ncclGroupEnd had not yet enqueued what its neighbours waited for
-    // (DESIGN.md §12). Before the ops of stage k the host waits until this rank's ops of
-    // stage k - window are done; the window exceeds the lag between neighbouring ranks'
-    // stage numbers (2 + d W), so every rank can always advance.
-    const bool windowed = c->NG > 1 && !c->peer;
-    int window = 16 + 4 * W;
-    if (const char* e = getenv("DSEA_NCCL_WINDOW"); e && *e) window = std::max(4, atoi(e));
-    struct StageMark { int stage; cudaEvent_t ev[3]; };
-    std::deque<StageMark> marks;
-    auto release_marks = [&]() { for (auto& m : marks) for (cudaEvent_t e : m.ev) cudaEventDestroy(e); marks.clear(); };
-    int cur_stage = -1;
     for (size_t oi = 0; oi < nops; oi++) {
         const Op& op = ops[oi];
-        if (windowed && op.stage != cur_stage) {
-            if (cur_stage >= 0) {                     // mark the end of the stage just enqueued
-                StageMark m{cur_stage, {nullptr, nullptr, nullptr}};
-                cudaStream_t sts[3] = {c->cs, c->ss, c->rs};
-                for (int k = 0; k < 3; k++) {
-                    cudaEventCreateWithFlags(&m.ev[k], cudaEventDisableTiming);
-                    cudaEventRecord(m.ev[k], sts[k]);
-                }
-                marks.push_back(m);
-            }
-            cur_stage = op.stage;
-            while (!marks.empty() && marks.front().stage <= cur_stage - window) {
-                for (cudaEvent_t e : marks.front().ev) {
-                    cudaError_t r = cudaEventSynchronize(e);
-                    cudaEventDestroy(e);
-                    if (r != cudaSuccess) { marks.pop_front(); release_marks(); return fail(c, DSEA_ECUDA, "stage window: %s", cudaGetErrorString(r)); }
-                }
-                marks.pop_front();
-            }
-        }
         switch (op.kind) {
         case OP_RECV: {
             if (c->peer) {  // data arrives by remote stores; just count the expected arrival
@@ -1279,7 +1245,6 @@ dsea_status run_plan(dsea_ctx* c, int64_t n_steps)
         }
         }
     }
-    release_marks();                   // (their waits are covered by the step's final synchronize)
     if (c->peer && c->rank == 0) {  // the final super-cycle lands in rank 0's input buffer
         if (c->ctr) {
             if (c->exp_arr[ns - 1] > 0) {
