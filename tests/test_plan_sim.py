@@ -138,3 +138,58 @@ def test_pushes_leave_in_slot_order(ns, ng, W, B):
             assert len(p) == cycles * ns
             recv = [int(o[3]) for o in plans[(r + 1) % ng] if int(o[0]) == R]
             assert recv == [s for _, s in p]      # (rank 0 also takes the last cycle back, Q22)
+
+
+def _staging_pool_hazards(ops, ns, pool, seq=True):
+    """Walk one rank's ops in stream order (force passes and bins run on the compute
+    stream in plan order): a FORCE (worker w, cycle K, slices [j, j+n)) writes staging
+    entries (K, j..j+n-1) of worker w into slots (K N_S + s) mod pool; a BIN of cycle K
+    over [m, m+n) reads (K, max(m-1, 0) .. min(m+n, N_S-1)) (atoms move at most one
+    slice per step).  Returns the writes that land on a slot whose current occupant
+    still has a read ahead of it."""
+    ops = [tuple(int(v) for v in o) for o in ops]
+    last_read = {}                               # (w, K, s) -> index of the last BIN reading it
+    for i, (kind, _, w, j, n, K, _) in enumerate(ops):
+        if kind == BN:
+            for s in range(max(j - 1, 0), min(j + n, ns - 1) + 1):
+                last_read[(w, K, s)] = i
+    occupant = {}                                # (w, slot) -> (K, s)
+    bad = []
+    for i, (kind, _, w, j, n, K, _) in enumerate(ops):
+        if kind != F:
+            continue
+        for s in range(j, j + n):
+            slot = (K * ns + s) % pool if seq else s % pool
+            prev = occupant.get((w, slot))
+            if prev is not None and prev != (K, s) and last_read.get((w, *prev), -1) > i:
+                bad.append((i, (K, s), prev))
+            occupant[(w, slot)] = (K, s)
+    return bad
+
+
+@pytest.mark.parametrize("ns,ng,W,B", CASES[::3] + BENCH_CASES)
+def test_staging_pool_size_never_overwrites_a_live_slice(ns, ng, W, B):
+    """NEXT-3 slot pools: a staged-schedule worker's staging buffer holds
+    2 B_max + 4 slices in slots that follow the global sequence number K N_S + j, with no
+    runtime guard -- only the compute stream's order.  For every plan (rings of 1-8
+    ranks, W workers, B slices per stage, partial super-cycles), no force pass may
+    overwrite a staging slot whose occupant a later bin still reads.  The same plans
+    with slot = j mod pool (no sequence number) do overwrite: the previous super-cycle's
+    last slice is binned after the next cycle's first block."""
+    for n_steps in (ng * W * 2 + 1, ng * W * 3):
+        for r in range(ng):
+            ops = D.dsea_plan_ops(ns, ng, r, W, n_steps, B)
+            bmax = max(int(o[4]) for o in ops if int(o[0]) == F)
+            pool = min(ns, 2 * bmax + 4)
+            assert not _staging_pool_hazards(ops, ns, pool), (ns, ng, W, B, r, n_steps)
+
+
+def test_staging_pool_needs_the_sequence_number():
+    """The negative control of the test above: with slot = j mod pool the last slice of
+    one super-cycle and the first block of the next collide (found on B200 as a failing
+    staged ring of one: P8, W = 1, B = 3)."""
+    ns, ng, W, B = 32, 1, 1, 3
+    ops = D.dsea_plan_ops(ns, ng, 0, W, 7, B)
+    pool = 2 * B + 4
+    assert _staging_pool_hazards(ops, ns, pool, seq=False)
+    assert not _staging_pool_hazards(ops, ns, pool, seq=True)
