@@ -652,14 +652,25 @@ k_bin_place(Geo g, BufView out, StgView stg, int s0, int flat_count, int m0, int
     if (flat_count > 0) { base = 0; n = flat_count; }
     else { const int s = s0 + blockIdx.y; base = wrap_slot(s + stg.soff, stg.pool) * g.cap; n = stg.n[s]; }
     const int p = blockIdx.x * PLACE_THREADS + threadIdx.x;
-    if (p >= n) return;
-    const int key = stg.key[base + p];
-    if (key < 0) return;
-    const int m = key / g.ncell;
-    if (m < m0 || m >= m0 + nm) return;
-    const int c = key - m * g.ncell;
-    const int pos = atomicAdd(&out.cnt[(size_t)m * g.ncell + c], 1);
-    if (pos < g.cap) {
+    const int lane = threadIdx.x & 31;
+    int key = -1, m = 0;
+    if (p < n) {
+        key = stg.key[base + p];
+        if (key >= 0) {
+            m = key / g.ncell;
+            if (m < m0 || m >= m0 + nm) key = -1;
+        }
+    }
+    // warp-aggregated cursor: consecutive staged atoms come from one source cell and
+    // mostly stay in one destination cell, so the lanes of a key share one atomicAdd
+    // (their order within the cell is irrelevant: the gather ranks a cell by (z, id))
+    const unsigned peers = __match_any_sync(FULLMASK, key >= 0 ? key : -2 - lane);
+    const int leader = __ffs(peers) - 1;
+    int pos = 0;
+    if (key >= 0 && lane == leader)
+        pos = atomicAdd(&out.cnt[(size_t)key], __popc(peers));   // key = m ncell + cell
+    pos = __shfl_sync(FULLMASK, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+    if (key >= 0 && pos < g.cap) {
         // the sort keys travel with the index (coalesced reads here), so the gather
         // ranks a cell without a dependent round trip to staging
         BinRec r;
