@@ -178,6 +178,9 @@ def run_reference(args, cfg, rank, world):
             "config": {"workload": cfg.name, "n_atoms": n, "n_slices": g.n_slices, "rho": cfg.rho,
                        "rc": cfg.rc},
             "impl": "reference",
+            "comparability": "not the same work as the GPU arm: Algorithm 1 forces of sampled atoms on the "
+                             "unmelted lattice (no kick, drift, migration or binning), while the GPU arm "
+                             "times the full step on a melted state; an upper bound of the oracle's rate",
             "cpu_baseline": {"value": value, "unit": "atom-timesteps/s", "cores": threads,
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "atom-timesteps/s", "h2d_bytes_per_step": 0,
