@@ -5,12 +5,13 @@
 // [j0, j0 + nj), each reading its left and right neighbour slices (O_in = 1).
 //
 // A tile is up to TILE_ATOMS consecutive, z-sorted home atoms of one (cx, cy) column of
-// slice j.  Persistent CTAs (a few per SM) claim tiles from a counter; per tile:
+// slice j.  Persistent CTAs (2 of 8 warps per SM at rho 0.8, rc 2.5) claim tiles from a
+// counter; per tile:
 //   1. a piece table: 9 neighbour columns x {low z-image, main run, high z-image}, the
 //      cells within one cell (l >= rc) of the home atoms' cells (periodic images in y
-//      and z pre-shifted, x walls: absent columns, readings Q1/Q2).  Warp 0
-//      builds the NEXT tile's table while the CTA works on the current one, so the
-//      dependent cell_start loads never stall the CTA;
+//      and z pre-shifted, x walls: absent columns, readings Q1/Q2).  The first
+//      warp out of chunks builds the NEXT tile's table while the others still work on
+//      the current one, so the dependent cell_start loads never stall the CTA;
 //   2. all warps stage the pieces into shared memory twice: FP64 (x, y, z) for the exact
 //      pair work and an FP32 screening record (x, y, z, w = x^2+y^2+z^2) relative to the
 //      tile centre, two atoms per 32 bytes so that one pair of LDS.128 feeds a packed
