@@ -193,3 +193,41 @@ def test_staging_pool_needs_the_sequence_number():
     pool = 2 * B + 4
     assert _staging_pool_hazards(ops, ns, pool, seq=False)
     assert not _staging_pool_hazards(ops, ns, pool, seq=True)
+
+
+def _nccl_sim():
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts", "nccl_plan_sim.py")
+    spec = importlib.util.spec_from_file_location("nccl_plan_sim", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def _degenerate(ns, B):
+    return -(-ns // B) <= 2          # one or two blocks per super-cycle
+
+
+@pytest.mark.parametrize("ns,ng,W,B", [c for c in CASES[::5] if c[1] > 1 and not _degenerate(c[0], c[3])]
+                         + [(32, 4, 2, 3), (32, 4, 1, 5)])
+def test_nccl_plans_have_no_stream_level_deadlock(ns, ng, W, B):
+    """The NCCL comparison backend's streams (compute, send, receive) with event waits
+    bound at enqueue time and rendezvous p2p groups matched in posting order
+    (`scripts/nccl_plan_sim.py`): every plan with more than two blocks per super-cycle
+    completes -- including the two 4-GPU plateau cases that hang on B200, whose hang is
+    therefore not a stream-level cycle of the plan (the ranks that never return block on
+    the host inside NCCL).  With one or two blocks per super-cycle at the
+    plateau the model does deadlock (grouped rendezvous sends; the peer backend, which
+    needs no rendezvous, completes them): a limitation of the comparison backend only --
+    the automatic block size always gives >= N_GPU (2 + W) - 1 blocks."""
+    sim = _nccl_sim()
+    for n_steps in (ng * W, ng * W * 2 + 1):
+        assert not sim.simulate(ns, ng, W, n_steps, B), (ns, ng, W, B, n_steps)
+
+
+def test_nccl_model_finds_the_degenerate_plateau_deadlock():
+    """Negative control of the NCCL stream model: 16 slices in blocks of 8 on a ring of 3
+    (two blocks per super-cycle, a partial last cycle) deadlocks under rendezvous
+    semantics -- so the model can find a cycle when there is one."""
+    assert _nccl_sim().simulate(16, 3, 1, 7, 8)
