@@ -235,3 +235,20 @@ def test_xprofile_compute_matches_oracle_pressure():
     assert np.allclose(x["x"], (np.arange(8) + 0.5) * g.w)
     assert np.allclose(x["u"][ok], -2900.0 / 500.0) and x["u"][3] == 0.0 and x["T"][3] == 0.0
     assert np.allclose(x["rho"], raw["n_sum"] / 10 / vol)
+
+
+def test_next3_billion_atom_geometry_fits_four_b200s():
+    """NEXT-3 (10^9 molecules, the N_i = 630 cube): the paper's slicing rule
+    gives 430 slices of 2.33e6 atoms; geometry equals the oracle's; the input buffer of
+    N_S slots (76 B of carried state per slot atom, ~95 GB) plus slot pools fits one
+    180 GB B200 -- measured 101-102 GB per GPU (profiles/r02/next3_1e9/)."""
+    st, g = D.dsea_geometry_compute(630, 630, 630, 0.8, 2.5)
+    o = oracle.geometry(630, 630, 630, 0.8, 2.5, 0, 1)
+    assert st == 0 and o.feasible
+    assert g.n_atoms == 1_000_188_000 == o.n_atoms
+    assert g.n_slices == o.n_slices == 430
+    assert g.slot_capacity >= 1.25 * g.n_atoms / g.n_slices and g.slot_capacity % 32 == 0
+    input_buffer = g.n_slices * g.slot_capacity * 76
+    assert 90e9 < input_buffer < 100e9
+    # Eq. (1): N_max = N_S / (2 + 2W) = 107 GPUs at W = 1 -- a ring of 4 is far from the plateau
+    assert g.n_max == 430 // 4
